@@ -1,0 +1,154 @@
+"""Generate the golden fixtures in tests/golden/ FROM THE REFERENCE ITSELF.
+
+Run in the development container, where /root/reference exists:
+
+    make -C oracle all ref && python tests/golden/make_golden.py
+
+It loads oracle/_ref/libhoodref.so (the unmodified reference sources compiled
+by oracle/Makefile, plus the extern "C" shim oracle/ref_shim.cpp) and records:
+
+  acceptance.npz  acceptance.cpp:44-72 sweep (seed 0xACCE97 + s*1315423911 + n),
+                  n = 4..1024, 8 seeds per size: the validated inputs, the
+                  hood::build_hood hull, and (n <= 256) the REMOTE-padded buffer
+                  after every round (on_round_end, acceptance criterion 2).
+  driver.npz      test_driver.cpp:61-70 sets (seed 900 + 31*s + n).
+  raw.npz         unvalidated uniform sets at n = 2^11..2^14 through the raw
+                  reference round loop (driver.cpp:20-43 steps), plus the
+                  reference upper_hull of the config generators at small n
+                  (grid 2^16, arc 2^14, gauss 2^16, batched 64 x 1024).
+  pairs.npz       make_random_hood_pair(d, 0xC4C5 + t) windows (acceptance.cpp:79)
+                  with the reference classify_g / classify_f tables and the
+                  merged block of match_and_merge_block (test_kernel.cpp:302-328).
+
+The fixtures are small (< 2 MB) and committed; the GPU box never needs the
+reference tree.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+import oracle as O  # noqa: E402
+from paper_1203_5004_b200 import workloads as W  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def acceptance():
+    data = {}
+    for n in [4, 8, 16, 32, 64, 128, 256, 512, 1024]:
+        pts, hulls, counts, rounds = [], [], [], []
+        for s in range(8):
+            seed = 0xACCE97 + s * 1315423911 + n
+            p = O.ref_make_random_point_set(n, seed)
+            h, rb = O.ref_build_hood(p, rounds=(n <= 256))
+            pad = np.zeros((n, 2))
+            pad[:, 0] = 10.0
+            pad[: len(h)] = h
+            pts.append(p)
+            hulls.append(pad)
+            counts.append(len(h))
+            if rb is not None:
+                rounds.append(rb)
+        data[f"pts_{n}"] = np.stack(pts)
+        data[f"hull_{n}"] = np.stack(hulls)
+        data[f"count_{n}"] = np.array(counts, dtype=np.int32)
+        if rounds:
+            data[f"rounds_{n}"] = np.stack(rounds)
+    np.savez_compressed(os.path.join(OUT, "acceptance.npz"), **data)
+
+
+def driver():
+    data = {}
+    for n in [4, 8, 32, 128, 256]:
+        pts, hulls, counts = [], [], []
+        for s in range(8):
+            p = O.ref_make_random_point_set(n, 900 + 31 * s + n)
+            h, _ = O.ref_build_hood(p)
+            pad = np.zeros((n, 2))
+            pad[:, 0] = 10.0
+            pad[: len(h)] = h
+            pts.append(p)
+            hulls.append(pad)
+            counts.append(len(h))
+        data[f"pts_{n}"] = np.stack(pts)
+        data[f"hull_{n}"] = np.stack(hulls)
+        data[f"count_{n}"] = np.array(counts, dtype=np.int32)
+    np.savez_compressed(os.path.join(OUT, "driver.npz"), **data)
+
+
+def raw():
+    data = {}
+    rng = np.random.default_rng(20260)
+    for e in [11, 12, 13, 14]:
+        n = 1 << e
+        x = np.sort(rng.random(n))
+        assert np.all(np.diff(x) > 0)
+        p = np.stack([x, rng.random(n)], axis=1)
+        data[f"uniform_pts_{n}"] = p
+        data[f"uniform_hull_{n}"] = O.ref_build_hood_raw(p)
+        assert np.array_equal(data[f"uniform_hull_{n}"], O.ref_upper_hull(p))
+    # Reference upper_hull of the config generators (inputs are regenerated
+    # by the tests from (n, seed); only the hulls are stored).
+    g = W.grid_uniform(1 << 16, seed=1)
+    data["grid65536_hull"] = O.ref_upper_hull(g.astype(np.float64))
+    a = W.arc(1 << 14)
+    data["arc16384_count"] = np.array([len(O.ref_upper_hull(a))])
+    gs = W.gauss(1 << 16, seed=4)
+    data["gauss65536_hull"] = O.ref_upper_hull(gs)
+    b = W.batched(64, 1024, seed=5)
+    bo, bc = O.ref_block_hulls(b.astype(np.float64), 1024)
+    data["batched64_counts"] = bc
+    data["batched64_slots"] = np.concatenate([bo[i * 1024: i * 1024 + bc[i]] for i in range(64)])
+    np.savez_compressed(os.path.join(OUT, "raw.npz"), **data)
+
+
+def pairs():
+    sizes = [2, 4, 8, 16, 32, 64]
+    slots, pq, g_tab, f_tab, merged, scratch01 = [], [], [], [], [], []
+    for t in range(120):
+        d = sizes[t % 6]
+        s, pc, qc = O.ref_make_random_hood_pair(d, 0xC4C5 + t)
+        w = np.zeros((128, 2))
+        w[:, 0] = 10.0
+        w[: 2 * d] = s
+        gt = np.full((64, 64), 9, dtype=np.int8)
+        ft = np.full((64, 64), 9, dtype=np.int8)
+        for i in range(pc):
+            for j in range(d, 2 * d):
+                gt[i, j - d] = O.ref().ref_classify_g(O._ptr(np.ascontiguousarray(s)), 2 * d, i, j, 0, d)
+        for j in range(qc):
+            for i in range(d):
+                ft[i, j] = O.ref().ref_classify_f(O._ptr(np.ascontiguousarray(s)), 2 * d, i, d + j, 0, d)
+        d1 = 1 << ((int(np.log2(d)) + 1) // 2)
+        d2 = d // d1
+        nh, sc = O.ref_merge_block(s, d1, d2)
+        m = np.zeros((128, 2))
+        m[:, 0] = 10.0
+        m[: 2 * d] = nh
+        slots.append(w)
+        pq.append((d, pc, qc))
+        g_tab.append(gt)
+        f_tab.append(ft)
+        merged.append(m)
+        scratch01.append(sc[:2])
+    np.savez_compressed(os.path.join(OUT, "pairs.npz"), slots=np.stack(slots), pq=np.array(pq, dtype=np.int32),
+                        g=np.stack(g_tab), f=np.stack(f_tab), merged=np.stack(merged),
+                        scratch01=np.stack(scratch01))
+
+
+if __name__ == "__main__":
+    O.build(ref=True)
+    acceptance()
+    driver()
+    raw()
+    pairs()
+    for f in sorted(os.listdir(OUT)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(OUT, f)))
