@@ -1,0 +1,111 @@
+/*
+ * hood_b200.h -- C-ABI of the B200-native upper-hood (upper convex hull)
+ * build.  Drop-in replacement for the reference's hot path
+ *
+ *     hood::build_hood(const PointSet&, const BuildOptions&) -> BuildReport
+ *         /root/reference/proj/include/hood/driver.hpp:43-45, src/driver.cpp:19-45
+ *
+ * and for its serial twin hood::oracle::upper_hull (oracle.hpp:23,
+ * oracle.cpp:7-20), whose result the reference's build must reproduce
+ * exactly (acceptance.cpp criterion 1).
+ *
+ * Plain pointers and sizes only.  Points are {x, y} pairs interleaved
+ * (the reference's Point2 layout, geom.hpp:7-12), x strictly increasing
+ * inside every instance.  Corners are returned left to right and are
+ * bit-identical copies of input points.
+ *
+ * Every entry point returns a hood_status; device-side failures
+ * (x not increasing, x out of range) are reported by hood_last_error(),
+ * which synchronizes the stream of the last build.
+ */
+#ifndef HOOD_B200_H
+#define HOOD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HOOD_B200_ABI_VERSION 1
+
+typedef struct hood_ctx hood_ctx;
+
+typedef enum hood_status {
+  HOOD_OK = 0,
+  HOOD_ERR_INVALID_ARG = 1,      /* bad size / alignment / block_len     */
+  HOOD_ERR_X_NOT_INCREASING = 2, /* ValidationError::x_not_increasing    */
+  HOOD_ERR_X_OUT_OF_RANGE = 3,   /* ValidationError::x_out_of_range      */
+  HOOD_ERR_DEGENERATE = 4,       /* reserved: DegenerateTangent          */
+  HOOD_ERR_CUDA = 5,             /* a CUDA runtime call failed           */
+  HOOD_ERR_CAPACITY = 6          /* workspace / record capacity exceeded */
+} hood_status;
+
+/* hoodbuf.hpp:18-32 ValidationError / kernel.hpp:98-102 DegenerateTangent. */
+typedef struct hood_error {
+  int32_t code;       /* hood_status                                    */
+  int32_t cuda_error; /* cudaError_t when code == HOOD_ERR_CUDA          */
+  int64_t index;      /* first offending point index (validation)       */
+} hood_error;
+
+/* Build flags. */
+#define HOOD_FLAG_CHECK_RANGE 0x1u /* also reject x outside (0, 1) (validate_points) */
+
+/* One context per device and host thread (the reference build is reentrant,
+ * SPEC.md:423; contexts share nothing). */
+int hood_create(hood_ctx** ctx, int device);
+int hood_destroy(hood_ctx* ctx);
+
+/* Pre-size the device workspace so later builds of at most n points never
+ * allocate (required before CUDA-graph capture). */
+int hood_reserve(hood_ctx* ctx, int64_t n, int64_t block_len, int f64);
+
+/* Device-pointer build, asynchronous on `stream` (a cudaStream_t, NULL = the
+ * legacy default stream).
+ *   d_pts      n points (2n scalars), 16-byte aligned.
+ *   block_len  0 or n: one instance (any n >= 1).  Otherwise a power of two
+ *              dividing n: n/block_len independent instances (the batched
+ *              config; also the reference's per-round blocks of length d).
+ *   d_corners  n slots; instance i's corners land at [i*block_len, ...).
+ *   d_counts   one int32 per instance.
+ *   d_padded   optional (NULL to skip): n slots in the reference HoodBuffer
+ *              layout after the last round -- corners then REMOTE = (10, 0)
+ *              (geom.hpp:14, hoodbuf.hpp:57-79).
+ */
+int hood_build_f32(hood_ctx* ctx, const float* d_pts, int64_t n, int64_t block_len, float* d_corners,
+                   int32_t* d_counts, float* d_padded, uint32_t flags, void* stream);
+int hood_build_f64(hood_ctx* ctx, const double* d_pts, int64_t n, int64_t block_len, double* d_corners,
+                   int32_t* d_counts, double* d_padded, uint32_t flags, void* stream);
+
+/* Host-pointer build (the reference-facing call: points in host memory,
+ * compact corners back in host memory).  Copies in pinned chunks overlapped
+ * with the slab kernels.  Synchronous.  h_corners needs n slots; returns the
+ * per-instance counts in h_counts. */
+int hood_build_host_f32(hood_ctx* ctx, const float* h_pts, int64_t n, int64_t block_len, float* h_corners,
+                        int32_t* h_counts, uint32_t flags);
+int hood_build_host_f64(hood_ctx* ctx, const double* h_pts, int64_t n, int64_t block_len,
+                        double* h_corners, int32_t* h_counts, uint32_t flags);
+
+/* Final merge of G adjacent x-slab hoods (the multi-GPU exchange step):
+ * segment g holds d_counts[g] corners at d_seg_pts + 2*g*seg_stride, slabs
+ * left to right.  Writes the hood of the union to d_corners (capacity
+ * G*seg_stride slots) and its size to d_count.  Asynchronous on `stream`. */
+int hood_merge_segments_f32(hood_ctx* ctx, const float* d_seg_pts, const int32_t* d_counts, int64_t G,
+                            int64_t seg_stride, float* d_corners, int32_t* d_count, void* stream);
+int hood_merge_segments_f64(hood_ctx* ctx, const double* d_seg_pts, const int32_t* d_counts, int64_t G,
+                            int64_t seg_stride, double* d_corners, int32_t* d_count, void* stream);
+
+/* Synchronizes the stream of the last build and reports its first error. */
+int hood_last_error(hood_ctx* ctx, hood_error* out);
+
+/* Number of kernels the last build enqueued (bench bookkeeping). */
+int hood_last_launch_count(hood_ctx* ctx);
+
+const char* hood_status_string(int status);
+int hood_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HOOD_B200_H */

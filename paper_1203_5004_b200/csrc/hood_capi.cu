@@ -1,0 +1,468 @@
+// C-ABI of the B200 upper-hood build (include/hood_b200.h).
+//
+// Host-side mirror of the reference driver (driver.cpp:19-45): where the
+// reference loops over log2(n)-1 rounds on the host, this layer plans ONE
+// slab launch (+ one finalize launch when an instance spans several slabs)
+// and never synchronizes inside a build, so builds can be captured into CUDA
+// graphs and the reference's per-round host<->device traffic
+// disappears.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/hood_b200.h"
+#include "hood_device.cuh"
+#include "hood_kernels.cuh"
+
+using namespace hood_b200;
+
+struct hood_ctx {
+  int device = 0;
+  int sms = 148;
+  // device workspace
+  int* seg_cnt = nullptr;
+  void* seg_ymax = nullptr;  // double-sized slots (fits float too)
+  long long* seg_base = nullptr;
+  long long seg_cap = 0;
+  DevError* err = nullptr;
+  // host-path buffers
+  void* d_in = nullptr;
+  size_t d_in_bytes = 0;
+  void* d_out = nullptr;
+  size_t d_out_bytes = 0;
+  int* d_counts = nullptr;
+  long long d_counts_cap = 0;
+  cudaStream_t s_copy = nullptr, s_comp = nullptr;
+  static constexpr int kChunks = 8;
+  cudaEvent_t ev[kChunks] = {};
+  // bookkeeping
+  cudaStream_t last_stream = nullptr;
+  bool have_last = false;
+  int last_launches = 0;
+  int sticky_cuda = 0;
+};
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return g_encode;
+}
+
+struct Plan {
+  bool hmode = true;
+  long long n = 0, L = 0, instances = 1, tiles = 0, tpi = 0;
+  int spi = 1;
+  long long units = 0, tpu = 1;
+  int grid = 0;
+  int seg_chunks = 256;
+};
+
+template <class S>
+int make_plan(hood_ctx* ctx, long long n, long long block_len, Plan& pl) {
+  constexpr int K = PointT<S>::K;
+  constexpr long long T = (long long)kThreads * K;
+  if (n < 1) return HOOD_ERR_INVALID_ARG;
+  pl.n = n;
+  pl.L = (block_len <= 0 || block_len == n) ? n : block_len;
+  if (pl.L != n) {
+    if ((pl.L & (pl.L - 1)) != 0 || n % pl.L != 0 || pl.L < K) return HOOD_ERR_INVALID_ARG;
+  }
+  pl.instances = n / pl.L;
+  pl.tiles = (n + T - 1) / T;
+  const long long resident = (long long)slab_kernel_occupancy<S>() * ctx->sms;
+  if (pl.L == n || pl.L >= T) {
+    pl.hmode = true;
+    pl.seg_chunks = kThreads;
+    pl.tpi = (pl.L + T - 1) / T;
+    long long spi = resident / pl.instances;
+    spi = std::max(1LL, std::min(spi, std::min(pl.tpi, (long long)kMaxSlabsPerInstance)));
+    pl.spi = (int)spi;
+    pl.units = pl.instances * pl.spi;
+  } else {
+    pl.hmode = false;
+    pl.seg_chunks = (int)(pl.L / K);
+    pl.tpu = std::max(1LL, (pl.tiles + resident - 1) / resident);
+    pl.units = (pl.tiles + pl.tpu - 1) / pl.tpu;
+  }
+  pl.grid = (int)std::min(pl.units, resident);
+  return HOOD_OK;
+}
+
+int ensure_ws(hood_ctx* ctx, long long slabs) {
+  if (!ctx->err) {
+    if (cudaMalloc(&ctx->err, sizeof(DevError)) != cudaSuccess) return HOOD_ERR_CUDA;
+  }
+  if (slabs > ctx->seg_cap) {
+    cudaFree(ctx->seg_cnt);
+    cudaFree(ctx->seg_ymax);
+    cudaFree(ctx->seg_base);
+    const long long cap = std::max(slabs, 4096LL);
+    if (cudaMalloc(&ctx->seg_cnt, cap * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&ctx->seg_ymax, cap * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&ctx->seg_base, cap * sizeof(long long)) != cudaSuccess)
+      return HOOD_ERR_CUDA;
+    ctx->seg_cap = cap;
+  }
+  return HOOD_OK;
+}
+
+template <class S>
+int encode_map(const void* pts, long long n, CUtensorMap* map, long long* full_rows) {
+  constexpr int K = PointT<S>::K;
+  *full_rows = n / K;
+  std::memset(map, 0, sizeof(*map));
+  if (*full_rows == 0) return HOOD_OK;
+  auto enc = encoder();
+  if (!enc) return HOOD_ERR_CUDA;
+  const cuuint64_t gdim[2] = {128, (cuuint64_t)*full_rows};
+  const cuuint64_t gstride[1] = {128};
+  const cuuint32_t box[2] = {128, (cuuint32_t)kThreads};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(pts), gdim, gstride, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? HOOD_OK : HOOD_ERR_CUDA;
+}
+
+template <class S>
+SlabParams<S> slab_params(hood_ctx* ctx, const Plan& pl, const void* pts, void* corners, int* counts,
+                          long long full_rows, uint32_t flags) {
+  SlabParams<S> p{};
+  p.pts = pts;
+  p.n = pl.n;
+  p.L = pl.L;
+  p.hmode = pl.hmode ? 1 : 0;
+  p.seg_chunks = pl.seg_chunks;
+  p.tiles_per_inst = pl.tpi;
+  p.slabs_per_inst = pl.spi;
+  p.num_units = pl.units;
+  p.tiles_per_unit = pl.tpu;
+  p.num_tiles = pl.tiles;
+  p.unit_lo = 0;
+  p.unit_hi = pl.units;
+  p.full_rows = full_rows;
+  p.out = corners;
+  p.out_counts = counts;
+  p.seg_cnt = ctx->seg_cnt;
+  p.seg_ymax = reinterpret_cast<S*>(ctx->seg_ymax);
+  p.seg_base = ctx->seg_base;
+  p.err = ctx->err;
+  p.check_range = (flags & HOOD_FLAG_CHECK_RANGE) ? 1 : 0;
+  return p;
+}
+
+template <class S>
+FinalizeParams<S> finalize_params(hood_ctx* ctx, const Plan& pl, void* corners, int* counts) {
+  using V = typename PointT<S>::V;
+  FinalizeParams<S> f{};
+  f.out = corners;
+  f.out_counts = counts;
+  f.seg_cnt = ctx->seg_cnt;
+  f.seg_ymax = reinterpret_cast<const S*>(ctx->seg_ymax);
+  f.seg_base = ctx->seg_base;
+  f.seg_stride = 0;
+  f.slabs_per_inst = pl.spi;
+  f.L = pl.L;
+  f.fcap = (int)((128 * 1024) / sizeof(V));
+  return f;
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+template <class S>
+int build_device(hood_ctx* ctx, const S* pts, long long n, long long block_len, S* corners, int* counts,
+                 S* padded, uint32_t flags, cudaStream_t st) {
+  if (!ctx || !pts || !corners || !counts) return HOOD_ERR_INVALID_ARG;
+  if (!aligned16(pts) || !aligned16(corners)) return HOOD_ERR_INVALID_ARG;
+  cudaSetDevice(ctx->device);
+  Plan pl;
+  int rc = make_plan<S>(ctx, n, block_len, pl);
+  if (rc) return rc;
+  if ((rc = ensure_ws(ctx, pl.units))) return rc;
+  CUtensorMap map;
+  long long full_rows = 0;
+  if ((rc = encode_map<S>(pts, n, &map, &full_rows))) return rc;
+  if (cudaMemsetAsync(ctx->err, 0xff, sizeof(DevError), st) != cudaSuccess) return HOOD_ERR_CUDA;
+  const SlabParams<S> p = slab_params<S>(ctx, pl, pts, corners, counts, full_rows, flags);
+  launch_slab_kernel<S>(p, &map, pl.grid, st);
+  int launches = 1;
+  if (pl.hmode && pl.spi > 1) {
+    launch_finalize<S>(finalize_params<S>(ctx, pl, corners, counts), (int)pl.instances, st);
+    ++launches;
+  }
+  if (padded) {
+    launch_pad_fill<S>(padded, corners, counts, n, pl.L, st);
+    ++launches;
+  }
+  const cudaError_t e = cudaGetLastError();
+  ctx->last_stream = st;
+  ctx->have_last = true;
+  ctx->last_launches = launches;
+  if (e != cudaSuccess) {
+    ctx->sticky_cuda = (int)e;
+    return HOOD_ERR_CUDA;
+  }
+  return HOOD_OK;
+}
+
+int decode_error(hood_ctx* ctx, hood_error* out) {
+  hood_error e{HOOD_OK, 0, -1};
+  if (ctx->sticky_cuda) {
+    e.code = HOOD_ERR_CUDA;
+    e.cuda_error = ctx->sticky_cuda;
+    ctx->sticky_cuda = 0;
+  } else if (ctx->have_last && ctx->err) {
+    cudaError_t ce = cudaStreamSynchronize(ctx->last_stream);
+    DevError de{~0ULL};
+    if (ce == cudaSuccess) ce = cudaMemcpy(&de, ctx->err, sizeof(de), cudaMemcpyDeviceToHost);
+    if (ce != cudaSuccess) {
+      e.code = HOOD_ERR_CUDA;
+      e.cuda_error = (int)ce;
+    } else if (de.key != ~0ULL) {
+      e.code = (de.key & 1ULL) ? HOOD_ERR_X_NOT_INCREASING : HOOD_ERR_X_OUT_OF_RANGE;
+      e.index = (int64_t)(de.key >> 1);
+    }
+  }
+  if (out) *out = e;
+  return e.code;
+}
+
+template <class S>
+int ensure_host_bufs(hood_ctx* ctx, long long n, long long instances) {
+  const size_t bytes = (size_t)n * 2 * sizeof(S);
+  if (bytes > ctx->d_in_bytes) {
+    cudaFree(ctx->d_in);
+    cudaFree(ctx->d_out);
+    ctx->d_in = ctx->d_out = nullptr;
+    if (cudaMalloc(&ctx->d_in, bytes) != cudaSuccess || cudaMalloc(&ctx->d_out, bytes) != cudaSuccess)
+      return HOOD_ERR_CUDA;
+    ctx->d_in_bytes = ctx->d_out_bytes = bytes;
+  }
+  if (instances > ctx->d_counts_cap) {
+    cudaFree(ctx->d_counts);
+    if (cudaMalloc(&ctx->d_counts, instances * sizeof(int)) != cudaSuccess) return HOOD_ERR_CUDA;
+    ctx->d_counts_cap = instances;
+  }
+  if (!ctx->s_copy) {
+    cudaStreamCreateWithFlags(&ctx->s_copy, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&ctx->s_comp, cudaStreamNonBlocking);
+    for (auto& e : ctx->ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  }
+  return HOOD_OK;
+}
+
+// Reference-facing host call: H2D in chunks on a copy stream, each chunk's
+// slabs launched as soon as its bytes land, then finalize and D2H of the
+// compact corners only.
+template <class S>
+int build_host(hood_ctx* ctx, const S* h_pts, long long n, long long block_len, S* h_corners, int* h_counts,
+               uint32_t flags) {
+  using V = typename PointT<S>::V;
+  constexpr long long T = (long long)kThreads * PointT<S>::K;
+  if (!ctx || !h_pts || !h_corners || !h_counts) return HOOD_ERR_INVALID_ARG;
+  cudaSetDevice(ctx->device);
+  Plan pl;
+  int rc = make_plan<S>(ctx, n, block_len, pl);
+  if (rc) return rc;
+  if ((rc = ensure_ws(ctx, pl.units))) return rc;
+  if ((rc = ensure_host_bufs<S>(ctx, n, pl.instances))) return rc;
+  S* d_in = reinterpret_cast<S*>(ctx->d_in);
+  S* d_out = reinterpret_cast<S*>(ctx->d_out);
+  CUtensorMap map;
+  long long full_rows = 0;
+  if ((rc = encode_map<S>(d_in, n, &map, &full_rows))) return rc;
+  cudaStream_t sc = ctx->s_copy, sk = ctx->s_comp;
+  cudaMemsetAsync(ctx->err, 0xff, sizeof(DevError), sk);
+  SlabParams<S> p = slab_params<S>(ctx, pl, d_in, d_out, ctx->d_counts, full_rows, flags);
+  const int chunks = (pl.hmode && pl.instances == 1 && pl.units >= hood_ctx::kChunks) ? hood_ctx::kChunks : 1;
+  for (int c = 0; c < chunks; ++c) {
+    const long long u0 = pl.units * c / chunks, u1 = pl.units * (c + 1) / chunks;
+    long long p0, p1;
+    if (chunks == 1) {
+      p0 = 0;
+      p1 = n;
+    } else {
+      p0 = (u0 * pl.tpi / pl.spi) * T;
+      p1 = (u1 == pl.units) ? n : std::min(n, (u1 * pl.tpi / pl.spi) * T);
+    }
+    cudaMemcpyAsync(d_in + 2 * p0, h_pts + 2 * p0, (size_t)(p1 - p0) * sizeof(V), cudaMemcpyHostToDevice, sc);
+    cudaEventRecord(ctx->ev[c], sc);
+    cudaStreamWaitEvent(sk, ctx->ev[c], 0);
+    p.unit_lo = u0;
+    p.unit_hi = u1;
+    const long long units_c = u1 - u0;
+    launch_slab_kernel<S>(p, &map, (int)std::min<long long>(units_c, pl.grid), sk);
+  }
+  if (pl.hmode && pl.spi > 1)
+    launch_finalize<S>(finalize_params<S>(ctx, pl, d_out, ctx->d_counts), (int)pl.instances, sk);
+  cudaMemcpyAsync(h_counts, ctx->d_counts, pl.instances * sizeof(int), cudaMemcpyDeviceToHost, sk);
+  if (cudaStreamSynchronize(sk) != cudaSuccess) return HOOD_ERR_CUDA;
+  ctx->last_stream = sk;
+  ctx->have_last = true;
+  ctx->last_launches = chunks + ((pl.hmode && pl.spi > 1) ? 1 : 0);
+  hood_error err;
+  if ((rc = decode_error(ctx, &err))) return rc;
+  if (pl.instances == 1) {
+    cudaMemcpy(h_corners, d_out, (size_t)h_counts[0] * sizeof(V), cudaMemcpyDeviceToHost);
+  } else {
+    for (long long i = 0; i < pl.instances; ++i)
+      cudaMemcpyAsync(h_corners + 2 * i * pl.L, d_out + 2 * i * pl.L, (size_t)h_counts[i] * sizeof(V),
+                      cudaMemcpyDeviceToHost, sk);
+    cudaStreamSynchronize(sk);
+  }
+  return cudaGetLastError() == cudaSuccess ? HOOD_OK : HOOD_ERR_CUDA;
+}
+
+template <class S>
+int merge_segments(hood_ctx* ctx, const S* seg_pts, const int* counts, long long G, long long stride,
+                   S* corners, int* count, cudaStream_t st) {
+  using V = typename PointT<S>::V;
+  if (!ctx || !seg_pts || !counts || !corners || !count) return HOOD_ERR_INVALID_ARG;
+  if (G < 1 || G > kMaxSlabsPerInstance || stride < 1) return HOOD_ERR_INVALID_ARG;
+  cudaSetDevice(ctx->device);
+  int rc;
+  if ((rc = ensure_ws(ctx, G))) return rc;
+  if (seg_pts != corners &&
+      cudaMemcpyAsync(corners, seg_pts, (size_t)G * stride * sizeof(V), cudaMemcpyDeviceToDevice, st) !=
+          cudaSuccess)
+    return HOOD_ERR_CUDA;
+  cudaMemcpyAsync(ctx->seg_cnt, counts, G * sizeof(int), cudaMemcpyDeviceToDevice, st);
+  cudaMemsetAsync(ctx->err, 0xff, sizeof(DevError), st);
+  FinalizeParams<S> f{};
+  f.out = corners;
+  f.out_counts = count;
+  f.seg_cnt = ctx->seg_cnt;
+  f.seg_ymax = nullptr;
+  f.seg_base = nullptr;
+  f.seg_stride = stride;
+  f.slabs_per_inst = (int)G;
+  f.L = G * stride;
+  f.fcap = (int)((128 * 1024) / sizeof(V));
+  launch_finalize<S>(f, 1, st);
+  ctx->last_stream = st;
+  ctx->have_last = true;
+  ctx->last_launches = 1;
+  return cudaGetLastError() == cudaSuccess ? HOOD_OK : HOOD_ERR_CUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hood_create(hood_ctx** out, int device) {
+  if (!out) return HOOD_ERR_INVALID_ARG;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return HOOD_ERR_CUDA;
+  if (cudaSetDevice(device) != cudaSuccess) return HOOD_ERR_CUDA;
+  hood_ctx* c = new hood_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  if (!encoder()) {
+    delete c;
+    return HOOD_ERR_CUDA;
+  }
+  *out = c;
+  return HOOD_OK;
+}
+
+int hood_destroy(hood_ctx* c) {
+  if (!c) return HOOD_OK;
+  cudaSetDevice(c->device);
+  cudaFree(c->seg_cnt);
+  cudaFree(c->seg_ymax);
+  cudaFree(c->seg_base);
+  cudaFree(c->err);
+  cudaFree(c->d_in);
+  cudaFree(c->d_out);
+  cudaFree(c->d_counts);
+  if (c->s_copy) {
+    for (auto& e : c->ev) cudaEventDestroy(e);
+    cudaStreamDestroy(c->s_copy);
+    cudaStreamDestroy(c->s_comp);
+  }
+  delete c;
+  return HOOD_OK;
+}
+
+int hood_reserve(hood_ctx* ctx, int64_t n, int64_t block_len, int f64) {
+  if (!ctx) return HOOD_ERR_INVALID_ARG;
+  cudaSetDevice(ctx->device);
+  Plan pl;
+  const int rc = f64 ? make_plan<double>(ctx, n, block_len, pl) : make_plan<float>(ctx, n, block_len, pl);
+  if (rc) return rc;
+  return ensure_ws(ctx, std::max(pl.units, (long long)kMaxSlabsPerInstance));
+}
+
+int hood_build_f32(hood_ctx* ctx, const float* d_pts, int64_t n, int64_t block_len, float* d_corners,
+                   int32_t* d_counts, float* d_padded, uint32_t flags, void* stream) {
+  return build_device<float>(ctx, d_pts, n, block_len, d_corners, d_counts, d_padded, flags,
+                             reinterpret_cast<cudaStream_t>(stream));
+}
+
+int hood_build_f64(hood_ctx* ctx, const double* d_pts, int64_t n, int64_t block_len, double* d_corners,
+                   int32_t* d_counts, double* d_padded, uint32_t flags, void* stream) {
+  return build_device<double>(ctx, d_pts, n, block_len, d_corners, d_counts, d_padded, flags,
+                              reinterpret_cast<cudaStream_t>(stream));
+}
+
+int hood_build_host_f32(hood_ctx* ctx, const float* h_pts, int64_t n, int64_t block_len, float* h_corners,
+                        int32_t* h_counts, uint32_t flags) {
+  return build_host<float>(ctx, h_pts, n, block_len, h_corners, h_counts, flags);
+}
+
+int hood_build_host_f64(hood_ctx* ctx, const double* h_pts, int64_t n, int64_t block_len,
+                        double* h_corners, int32_t* h_counts, uint32_t flags) {
+  return build_host<double>(ctx, h_pts, n, block_len, h_corners, h_counts, flags);
+}
+
+int hood_merge_segments_f32(hood_ctx* ctx, const float* d_seg_pts, const int32_t* d_counts, int64_t G,
+                            int64_t seg_stride, float* d_corners, int32_t* d_count, void* stream) {
+  return merge_segments<float>(ctx, d_seg_pts, d_counts, G, seg_stride, d_corners, d_count,
+                               reinterpret_cast<cudaStream_t>(stream));
+}
+
+int hood_merge_segments_f64(hood_ctx* ctx, const double* d_seg_pts, const int32_t* d_counts, int64_t G,
+                            int64_t seg_stride, double* d_corners, int32_t* d_count, void* stream) {
+  return merge_segments<double>(ctx, d_seg_pts, d_counts, G, seg_stride, d_corners, d_count,
+                                reinterpret_cast<cudaStream_t>(stream));
+}
+
+int hood_last_error(hood_ctx* ctx, hood_error* out) {
+  if (!ctx) return HOOD_ERR_INVALID_ARG;
+  return decode_error(ctx, out);
+}
+
+int hood_last_launch_count(hood_ctx* ctx) { return ctx ? ctx->last_launches : 0; }
+
+const char* hood_status_string(int s) {
+  switch (s) {
+    case HOOD_OK: return "ok";
+    case HOOD_ERR_INVALID_ARG: return "invalid argument";
+    case HOOD_ERR_X_NOT_INCREASING: return "x not strictly increasing";
+    case HOOD_ERR_X_OUT_OF_RANGE: return "x outside (0, 1)";
+    case HOOD_ERR_DEGENERATE: return "degenerate tangent";
+    case HOOD_ERR_CUDA: return "CUDA error";
+    case HOOD_ERR_CAPACITY: return "capacity exceeded";
+  }
+  return "unknown";
+}
+
+int hood_abi_version(void) { return HOOD_B200_ABI_VERSION; }
+
+}  // extern "C"

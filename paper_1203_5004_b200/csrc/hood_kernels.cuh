@@ -1,0 +1,73 @@
+// Kernel parameter blocks and host launch entry points (internal to the
+// library; the public surface is the C-ABI in include/hood_b200.h).
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace hood_b200 {
+
+constexpr int kThreads = 256;       // one 128-byte chunk row per thread
+constexpr int kStages = 3;          // TMA pipeline depth per CTA
+constexpr int kTileBytes = kThreads * 128;
+constexpr int kHCap = 1024;         // running slab hull kept in smem up to this many corners
+constexpr int kMaxSlabsPerInstance = 1024;
+
+// First error of a build, encoded as key = index*2 + (x_not_increasing ? 1 : 0)
+// so one atomicMin keeps validate_points' order (hoodbuf.cpp:48-58: at the
+// same index the range check fires before the order check).
+struct DevError {
+  unsigned long long key;
+};
+
+template <class S>
+struct SlabParams {
+  const void* pts;          // n points, {x, y} interleaved, 16-byte aligned
+  long long n;
+  long long L;              // instance length (== n for a single instance)
+  int hmode;                // 1: slabs with a running hull; 0: whole instances per tile (L < T)
+  int seg_chunks;           // chunks per culling segment: 256 (hmode) or L/K
+  long long tiles_per_inst; // hmode: ceil(L / T)
+  int slabs_per_inst;       // hmode
+  long long num_units;      // hmode: slabs; else groups of tiles
+  long long tiles_per_unit; // !hmode
+  long long num_tiles;
+  long long unit_lo, unit_hi;  // units processed by this launch
+  long long full_rows;      // rows of the TMA tensor (n*sizeof(V)/128)
+  void* out;                // corner slots (n), instance i at [i*L, i*L+count)
+  int* out_counts;          // per instance
+  int* seg_cnt;             // per slab (hmode)
+  S* seg_ymax;
+  long long* seg_base;
+  DevError* err;
+  int check_range;          // also flag x outside (0,1) (validate_points)
+};
+
+template <class S>
+struct FinalizeParams {
+  void* out;
+  int* out_counts;
+  const int* seg_cnt;
+  const S* seg_ymax;        // nullptr: compute from the segment corners
+  const long long* seg_base; // nullptr: segment s starts at s * seg_stride
+  long long seg_stride;
+  int slabs_per_inst;
+  long long L;
+  int fcap;                 // smem corner capacity of the fast path
+};
+
+template <class S>
+void launch_slab_kernel(const SlabParams<S>& p, const CUtensorMap* tmap, int grid, cudaStream_t st);
+template <class S>
+void launch_finalize(const FinalizeParams<S>& p, int instances, cudaStream_t st);
+template <class S>
+void launch_pad_fill(void* padded, const void* corners, const int* counts, long long n, long long L,
+                     cudaStream_t st);
+template <class S>
+int slab_kernel_occupancy();
+template <class S>
+size_t slab_kernel_smem();
+size_t finalize_smem(int fcap_bytes, int slabs);
+
+}  // namespace hood_b200

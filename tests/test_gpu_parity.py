@@ -1,0 +1,304 @@
+"""GPU parity: libhood_b200.so (through the C-ABI) vs the pinned CPU oracle.
+
+Bit-exact comparison of corner coordinates (corners are selections of input
+points; hood_b200.h).  Golden vectors restate the reference's own tests with
+file:line; the fixtures come from the reference itself (tests/golden/).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+from paper_1203_5004_b200 import hood as H  # noqa: E402
+from paper_1203_5004_b200 import workloads as W  # noqa: E402
+
+R = (10.0, 0.0)
+A, B, C, D = (0.1, 0.5), (0.2, 0.6), (0.6, 0.9), (0.7, 0.2)
+
+
+def gpu_hull(pts, dtype=torch.float64, **kw):
+    t = torch.as_tensor(np.asarray(pts), dtype=dtype).cuda().contiguous()
+    return H.build_hood(t, **kw).hull.cpu().numpy()
+
+
+def same(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b, dtype=a.dtype)
+    return a.shape == b.shape and np.array_equal(a, b)
+
+
+# ------------------------------------------------------------ golden vectors
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_known_answers(dtype):
+    npd = np.float64 if dtype == torch.float64 else np.float32
+    cases = [
+        ([A, B, C, D], [A, B, C, D]),                                        # test_kernel.cpp:119-125
+        ([(0.1, 0.9), (0.3, 0.3), (0.6, 0.25), (0.9, 0.8)], [(0.1, 0.9), (0.9, 0.8)]),  # :127-132
+        ([A, B, (0.6, 0.1), (0.7, 0.2)], [A, B, (0.7, 0.2)]),                # :133-138
+        ([(0.2, 0.4), (0.6, 0.3)], [(0.2, 0.4), (0.6, 0.3)]),                # :141-151
+        ([(0.05, 0.5), (0.1, 0.45), (0.15, 0.35), (0.2, 0.2),
+          (0.8, 0.2), (0.85, 0.35), (0.9, 0.45), (0.95, 0.5)], [(0.05, 0.5), (0.95, 0.5)]),  # :153-168
+        ([(0.05, 0.05), (0.25, 0.09), (0.45, 0.1), (0.5, 0.05), (0.55, 0.3), (0.6, 0.35)],
+         [(0.05, 0.05), (0.6, 0.35)]),                                         # :269-300
+        ([(0.3, 0.4), (0.6, 0.2)], [(0.3, 0.4), (0.6, 0.2)]),                # test_driver.cpp:36-42
+        ([(0.5, 0.5)], [(0.5, 0.5)]),
+    ]
+    for pts, want in cases:
+        assert same(gpu_hull(pts, dtype), np.array(want, dtype=npd)), pts
+    par = [(k / 9.0, (k / 9.0) * (1.0 - k / 9.0)) for k in range(1, 9)]   # test_driver.cpp:51-59
+    assert same(gpu_hull(par, dtype), np.array(par, dtype=npd))
+    s8 = [(0.0625, 0.05859375), (0.125, 0.109375), (0.1875, 0.15234375), (0.25, 0.1875),
+          (0.3125, 0.21484375), (0.375, 0.234375), (0.4375, 0.24609375), (0.5, 0.25)]  # data/sample8.txt
+    assert same(gpu_hull(s8, dtype), np.array(s8, dtype=npd))
+
+
+def test_dyadic_degenerate_resolved_like_oracle(oracle_mod):
+    """test_kernel.cpp:330-350: the reference kernel flags this collinear
+    tangency; the oracle resolves it (collinear middle points dropped) and so
+    does the GPU path, bit for bit."""
+    pts = np.array([(0.0625, 0.25), (0.125, 0.4), (0.25, 0.5), (0.3125, 0.46875),
+                    (0.5625, 0.3), (0.625, 0.3125), (0.6875, 0.28), (0.75, 0.2)])
+    assert same(gpu_hull(pts), oracle_mod.upper_hull(pts))
+
+
+def test_acceptance_fixture_sweep(golden):
+    """acceptance.cpp:44-72 criterion 1 against hood::build_hood's own output."""
+    g = golden("acceptance.npz")
+    for n in [4, 8, 16, 32, 64, 128, 256, 512, 1024]:
+        pts = g[f"pts_{n}"]
+        for s in range(pts.shape[0]):
+            k = int(g[f"count_{n}"][s])
+            assert same(gpu_hull(pts[s]), g[f"hull_{n}"][s][:k]), (n, s)
+
+
+def test_driver_fixture(golden):  # test_driver.cpp:61-70
+    g = golden("driver.npz")
+    for n in [4, 8, 32, 128, 256]:
+        for s in range(8):
+            k = int(g[f"count_{n}"][s])
+            assert same(gpu_hull(g[f"pts_{n}"][s]), g[f"hull_{n}"][s][:k])
+
+
+def test_raw_reference_fixture(golden):
+    g = golden("raw.npz")
+    for e in [11, 12, 13, 14]:
+        n = 1 << e
+        assert same(gpu_hull(g[f"uniform_pts_{n}"]), g[f"uniform_hull_{n}"])
+    assert same(gpu_hull(W.grid_uniform(1 << 16, seed=1), torch.float32).astype(np.float64), g["grid65536_hull"])
+    assert same(gpu_hull(W.gauss(1 << 16, seed=4)), g["gauss65536_hull"])
+
+
+def test_per_round_blocks(golden, oracle_mod):
+    """acceptance criterion 2 / test_driver.cpp:72-94: every round-r block is
+    the hull of its interval -- the GPU batched mode with block_len = d."""
+    g = golden("acceptance.npz")
+    for n in [64, 128, 256]:
+        for s in range(4):
+            p = g[f"pts_{n}"][s]
+            t = torch.as_tensor(p).cuda()
+            for r, buf in enumerate(g[f"rounds_{n}"][s]):
+                d = 4 << r
+                if d < 8:
+                    continue
+                rep = H.build_hood(t, block_len=d, padded=True)
+                assert same(rep.padded.cpu().numpy(), buf), (n, s, d)
+
+
+# ------------------------------------------------------------ random / degenerate
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_random_sizes(oracle_mod, dtype):
+    rng = np.random.default_rng(11)
+    npd = np.float64 if dtype == torch.float64 else np.float32
+    for n in [1, 2, 3, 5, 15, 16, 17, 255, 256, 257, 1000, 4095, 4096, 4097, 8191, 20000, 65537, 300001,
+              1 << 20]:
+        x = np.sort(rng.random(n)).astype(npd)
+        ok = np.concatenate([[True], np.diff(x) > 0])
+        x, m = x[ok], int(ok.sum())
+        p = np.stack([x, rng.random(m).astype(npd)], axis=1)
+        assert same(gpu_hull(p, dtype), oracle_mod.upper_hull(p)), n
+
+
+def test_lattice_degenerate(oracle_mod):
+    """Exactly collinear triples everywhere (exact predicates): the strict hull
+    must match the oracle's pop-on-collinear rule."""
+    for seed in range(12):
+        for n, span in [(500, 16), (5000, 64), (70000, 256), (300000, 4096)]:
+            p = W.lattice(n, span, seed=seed)
+            assert same(gpu_hull(p), oracle_mod.upper_hull(p)), (seed, n)
+            p32 = p.astype(np.float32)
+            if np.all(np.diff(p32[:, 0]) > 0):
+                assert same(gpu_hull(p32, torch.float32), oracle_mod.upper_hull(p32)), (seed, n)
+
+
+def test_concave_and_convex_shapes(oracle_mod):
+    for n in [100, 5000, 70000, 1 << 18]:
+        a = W.arc(n)
+        assert same(gpu_hull(a), oracle_mod.upper_hull(a))
+        cup = a.copy()
+        cup[:, 1] = 1.0 - cup[:, 1]
+        assert same(gpu_hull(cup), oracle_mod.upper_hull(cup))
+        # arc with a dent: large hulls cut in the middle (global merge path)
+        dent = a.copy()
+        dent[n // 3: 2 * n // 3, 1] -= 0.2
+        assert same(gpu_hull(dent), oracle_mod.upper_hull(dent))
+
+
+# ------------------------------------------------------------ the five configs
+
+def test_config1_grid_2p16(oracle_mod):
+    p = W.grid_uniform(1 << 16, seed=1)
+    assert same(gpu_hull(p, torch.float32), oracle_mod.upper_hull(p))
+
+
+def test_config2_grid_2p24(oracle_mod):
+    t = W.grid_uniform_torch(1 << 24, seed=2)
+    got = H.build_hood(t).hull.cpu().numpy()
+    assert same(got, oracle_mod.upper_hull(t.cpu().numpy()))
+
+
+def test_config3_arc_2p22(oracle_mod):
+    t = W.arc_torch(1 << 22)
+    rep = H.build_hood(t)
+    assert int(rep.counts[0]) == 1 << 22
+    assert same(rep.hull.cpu().numpy(), oracle_mod.upper_hull(t.cpu().numpy()))
+
+
+def test_config4_gauss_2p26(oracle_mod):
+    t = W.gauss_torch(1 << 26, seed=4)
+    got = H.build_hood(t).hull.cpu().numpy()
+    assert same(got, oracle_mod.upper_hull(t.cpu().numpy()))
+
+
+@pytest.mark.slow
+def test_config4_gauss_2p28(oracle_mod):
+    t = W.gauss_torch(1 << 28, seed=4)
+    got = H.build_hood(t).hull.cpu().numpy()
+    host = t.cpu().numpy()
+    del t
+    assert same(got, oracle_mod.upper_hull(host))
+
+
+def test_config5_batched(oracle_mod):
+    t = W.batched_torch(65536, 1024, seed=5)
+    rep = H.build_hood(t, block_len=1024)
+    host = t.cpu().numpy()
+    slots, counts = oracle_mod.block_hulls(host, 1024)
+    gc = rep.counts.cpu().numpy()
+    assert np.array_equal(gc, counts)
+    gs = rep.corners.cpu().numpy()
+    mask = (np.arange(1024)[None, :] < counts[:, None]).reshape(-1)
+    assert np.array_equal(gs[mask], slots[mask])
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("block", [8, 16, 64, 256, 1024, 4096, 1 << 14, 1 << 16])
+def test_block_lengths(oracle_mod, dtype, block):
+    n = 1 << 20
+    if dtype == torch.float32 and block < 16:
+        pytest.skip("float2 chunks are 16 points")
+    p = W.batched(n // block, block, seed=block) if block <= (1 << 14) else None
+    if p is None:
+        p = np.concatenate([W.grid_uniform(block, seed=s) for s in range(n // block)])
+    p = p.astype(np.float64 if dtype == torch.float64 else np.float32)
+    t = torch.as_tensor(p).cuda()
+    rep = H.build_hood(t, block_len=block)
+    slots, counts = oracle_mod.block_hulls(p, block)
+    assert np.array_equal(rep.counts.cpu().numpy(), counts)
+    mask = (np.arange(block)[None, :] < counts[:, None]).reshape(-1)
+    assert np.array_equal(rep.corners.cpu().numpy()[mask], slots[mask])
+
+
+# ------------------------------------------------------------ boundary behaviour
+
+def test_padded_output(oracle_mod):
+    p = W.grid_uniform(1 << 16, seed=9)
+    t = torch.as_tensor(p).cuda()
+    rep = H.build_hood(t, padded=True)
+    h = oracle_mod.upper_hull(p)
+    pad = rep.padded.cpu().numpy()
+    assert np.array_equal(pad[: len(h)], h)
+    assert np.all(pad[len(h):, 0] == 10.0) and np.all(pad[len(h):, 1] == 0.0)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_x_not_increasing_reported(dtype):
+    for n, bad in [(8, 3), (5000, 4096), (5000, 4095), (1 << 20, 777777), (1 << 20, 1)]:
+        x = np.linspace(0.1, 0.9, n)
+        x[bad] = x[bad - 1]
+        p = np.stack([x, np.full(n, 0.5)], axis=1)
+        with pytest.raises(H.ValidationError) as ei:
+            gpu_hull(p, dtype)
+        assert ei.value.code == H.HOOD_ERR_X_NOT_INCREASING and ei.value.index == bad
+
+
+def test_x_range_check():
+    p = np.array([(0.1, 0.5), (1.2, 0.6)])
+    assert same(gpu_hull(p), p)  # the raw path (oracle::upper_hull) accepts it
+    with pytest.raises(H.ValidationError) as ei:
+        gpu_hull(p, check_range=True)
+    assert ei.value.code == H.HOOD_ERR_X_OUT_OF_RANGE and ei.value.index == 1
+
+
+def test_invalid_block_len():
+    t = torch.rand(100, 2, dtype=torch.float64).cuda()
+    with pytest.raises(H.HoodError):
+        H.build_hood(t, block_len=7)
+
+
+def test_host_path(oracle_mod):
+    for p in [W.grid_uniform(1 << 20, seed=3), W.gauss(1 << 20, seed=6), W.arc(1 << 16)]:
+        out, counts = H.build_hood_host(np.ascontiguousarray(p))
+        assert same(out[: counts[0]], oracle_mod.upper_hull(p))
+    b = W.batched(256, 1024, seed=8)
+    out, counts = H.build_hood_host(b, block_len=1024)
+    slots, oc = oracle_mod.block_hulls(b, 1024)
+    assert np.array_equal(counts, oc)
+
+
+@pytest.mark.parametrize("G", [2, 4, 8, 64])
+def test_merge_segments(oracle_mod, G):
+    """The multi-GPU exchange step on one device: per-slab hoods, then the
+    final merge (A10 shows slab hulls compose exactly)."""
+    for maker in [lambda: W.gauss(1 << 20, seed=G), lambda: W.arc(1 << 14)]:
+        p = maker()
+        n = p.shape[0]
+        slabs = np.array_split(p, G)
+        stride = max(len(s) for s in slabs)
+        seg = torch.zeros(G, stride, 2, dtype=torch.float64, device="cuda")
+        cnt = torch.zeros(G, dtype=torch.int32, device="cuda")
+        for g, s in enumerate(slabs):
+            h = H.build_hood(torch.as_tensor(np.ascontiguousarray(s)).cuda()).hull
+            seg[g, : h.shape[0]] = h
+            cnt[g] = h.shape[0]
+        out, c = H.merge_segments(seg, cnt)
+        torch.cuda.synchronize()
+        got = out[: int(c[0])].cpu().numpy()
+        assert same(got, oracle_mod.upper_hull(p)), (G, n)
+
+
+def test_graph_capture_replay(oracle_mod):
+    p = W.grid_uniform(1 << 20, seed=12)
+    t = torch.as_tensor(p).cuda()
+    ctx = H.Context.get(0)
+    ctx.reserve(t.shape[0])
+    corners = torch.empty_like(t)
+    counts = torch.empty(1, dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        H.build_hood_async(t, corners=corners, counts=counts)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        H.build_hood_async(t, corners=corners, counts=counts)
+    corners.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    h = oracle_mod.upper_hull(p)
+    assert int(counts[0]) == len(h)
+    assert same(corners[: len(h)].cpu().numpy(), h)
