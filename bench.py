@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""Benchmark of the upper-hood build -- BASELINE.json's headline metric.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
+
+A "step" is one build of the hood of one synthetic x-sorted point set that is
+already resident in HBM.  At N=1 the workload is config 2 (n = 2^24 uniform
+points on the 2^-24 float grid, float2 storage); under torchrun (N>1) every
+rank owns one contiguous x-slab of 2^24 points (weak scaling) and the step is
+slab build -> NCCL all_gather of the slab hoods -> final merge on every rank.
+
+value     = points of all ranks / step time (max over ranks), Gpoints/s
+e2e       = the same metric through the host-pointer C-ABI call
+            (hood_build_host_*: pinned host points -> H2D -> build -> D2H of
+            counts + corners), host copies inside the timed region
+roofline  = slab kernel (the dominant kernel): algorithmic bytes (8 B/pt
+            float2) / its CUDA-event duration, vs MEASURED_PEAKS.json hbm_gbs
+cpu_baseline = the reference's own oracle::upper_hull (oracle/_ref, compiled
+            from /root/reference sources) on one host core, full workload
+
+--impl reference: the reference CPU implementation of the path (oracle/_ref
+slab-parallel upper_hull, every host thread) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gpoints/sec upper-hood build (x-sorted float2) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "Gpoints/s"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--log2n", type=int, default=None, help="override n for configs 2/4")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload(cfg: int, log2n=None):
+    """(description, n, storage, block_len, builder(device|'cpu'))."""
+    from paper_1203_5004_b200 import workloads as W
+    if cfg == 1:
+        n = 1 << 16
+        return ("config1: n=2^16 uniform grid points, float2", n, "float2", 0,
+                lambda dev: W.grid_uniform_torch(n, seed=1, device=dev))
+    if cfg == 2:
+        n = 1 << (log2n or 24)
+        return (f"config2: n=2^{n.bit_length() - 1} uniform grid points in (0,1)^2, x-sorted, float2", n, "float2", 0,
+                lambda dev: W.grid_uniform_torch(n, seed=2, device=dev))
+    if cfg == 3:
+        n = 1 << 22
+        return ("config3: n=2^22 concave arc (every point a corner), double2", n, "double2", 0,
+                lambda dev: W.arc_torch(n, device=dev))
+    if cfg == 4:
+        n = 1 << (log2n or 28)
+        return (f"config4: n=2^{n.bit_length() - 1} Gaussian, x-sorted, double2", n, "double2", 0,
+                lambda dev: W.gauss_torch(n, seed=4, device=dev))
+    n = 65536 * 1024
+    return ("config5: 65536 instances x 1024 points, float2", n, "float2", 1024,
+            lambda dev: W.batched_torch(65536, 1024, seed=5, device=dev))
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(cfg: int):
+    """dram bytes per slab-kernel launch from the committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        return d.get(f"config{cfg}")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML SM clock / throttle sampling while the timed region runs."""
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._th = None
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+        except Exception:
+            self.N = None
+
+    def _run(self):
+        N = self.N
+        names = {
+            getattr(N, "nvmlClocksEventReasonHwSlowdown", 0x8): "hw_slowdown",
+            getattr(N, "nvmlClocksEventReasonHwThermalSlowdown", 0x40): "hw_thermal_slowdown",
+            getattr(N, "nvmlClocksEventReasonSwThermalSlowdown", 0x20): "sw_thermal_slowdown",
+            getattr(N, "nvmlClocksEventReasonSwPowerCap", 0x4): "sw_power_cap",
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, nm in names.items():
+                    if r & bit:
+                        self.reasons.add(nm)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.N is not None:
+            self._th = threading.Thread(target=self._run, daemon=True)
+            self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._th:
+            self._th.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def cpu_reference_rate(points_np, seconds: float, threads: int):
+    """Gpoints/s of the reference upper_hull (oracle/_ref if built, else the C port)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    import numpy as np
+    pts = np.ascontiguousarray(points_np, dtype=np.float64)
+    kind = "reference" if O.ref_available() else "port"
+    fn = (lambda: O.ref_upper_hull(pts, threads=threads)) if kind == "reference" else \
+        (lambda: O.upper_hull(pts, threads=threads))
+    times = []
+    t_end = time.perf_counter() + seconds
+    while True:
+        t0 = time.perf_counter()
+        fn()
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() > t_end and len(times) >= 1:
+            break
+    return pts.shape[0] / statistics.median(times) / 1e9, kind, len(times)
+
+
+def cpu_reference_batched_rate(points_np, block, seconds, threads):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    import numpy as np
+    pts = np.ascontiguousarray(points_np, dtype=np.float64)
+    kind = "reference" if O.ref_available() else "port"
+    times = []
+    t_end = time.perf_counter() + seconds
+    while True:
+        t0 = time.perf_counter()
+        if kind == "reference":
+            O.ref_block_hulls(pts, block, threads=threads)
+        else:
+            O.block_hulls(pts, block)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() > t_end:
+            break
+    return pts.shape[0] / statistics.median(times) / 1e9, kind, len(times)
+
+
+# ---------------------------------------------------------------- reference arm
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import numpy as np
+    desc, n, storage, block, make = workload(args.config, args.log2n)
+    pts = make("cpu").numpy()
+    threads = os.cpu_count() or 1
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    kind = "reference" if O.ref_available() else "port"
+    p64 = np.ascontiguousarray(pts, dtype=np.float64)
+    N = args.gpus
+
+    def step():
+        if block:
+            if kind == "reference":
+                O.ref_block_hulls(p64, block, threads=threads)
+            else:
+                O.block_hulls(p64, block)
+        else:
+            if kind == "reference":
+                O.ref_upper_hull(p64, threads=threads)
+            else:
+                O.upper_hull(p64, threads=threads)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    # Weak scaling: the reference has no multi-node layer; N slabs of n points
+    # on the same host cores cost N x the single-slab time.
+    value = n / dt / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 * N,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": desc, "n_per_rank": n, "storage": storage,
+                                        "block_len": block or n},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"full workload per step ({n} points), "
+                                   f"{'oracle/_ref' if kind == 'reference' else 'oracle port'} "
+                                   f"{'block' if block else 'slab'}-parallel upper_hull on {threads} threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- our arm
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_1203_5004_b200 import hood as H
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+
+    desc, n, storage, block, make = workload(args.config, args.log2n)
+    pts = make(dev)
+    f64 = pts.dtype == torch.float64
+    bpp = 16 if f64 else 8
+    ctx = H.Context.get(local)
+    ctx.reserve(n, block, f64)
+    corners = torch.empty_like(pts)
+    inst = n // block if block else 1
+    counts = torch.empty(inst, dtype=torch.int32, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    # multi-GPU exchange buffers (slab hoods in global double coordinates)
+    CAP = 4096
+    if world > 1:
+        rec = torch.zeros(CAP + 1, 2, dtype=torch.float64, device=dev)
+        gathered = torch.zeros(world, CAP + 1, 2, dtype=torch.float64, device=dev)
+        seg_cnt = torch.zeros(world, dtype=torch.int32, device=dev)
+        final = torch.empty(world * CAP, 2, dtype=torch.float64, device=dev)
+        final_cnt = torch.empty(1, dtype=torch.int32, device=dev)
+
+    def exchange():
+        # slab r lives at x in (r, r+1): shift the (float) slab hood into
+        # global double coordinates (exact), gather, merge on every rank.
+        k = counts[0]
+        idx = torch.arange(CAP, device=dev)
+        h = corners[:CAP].to(torch.float64)
+        h[:, 0] += rank
+        rec[1:] = torch.where((idx < k)[:, None], h, torch.zeros_like(h))
+        rec[0, 0] = k.to(torch.float64)
+        dist.all_gather_into_tensor(gathered.view(-1), rec.view(-1))
+        seg_cnt.copy_(gathered[:, 0, 0].to(torch.int32))
+        H.merge_segments(gathered[:, 1:, :].contiguous(), seg_cnt, out=final, out_count=final_cnt)
+
+    def one_step():
+        H.build_hood_async(pts, block, corners=corners, counts=counts)
+        if world > 1:
+            exchange()
+
+    # correctness gate before timing (one build vs the CPU oracle on rank 0)
+    one_step()
+    ctx.last_error()
+    if world > 1 and int(counts[0]) > CAP:
+        raise RuntimeError("slab hood exceeds the exchange record capacity")
+
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kb = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ka = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for e in kb + ka:  # torch creates the cudaEvent_t lazily, on first record
+        e.record(stream)
+    for _ in range(args.warmup):
+        flush.zero_()
+        one_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches = 0
+    sampler = ClockSampler(local)
+    with sampler:
+        for i in range(args.steps):
+            flush.zero_()
+            ctx.set_profile_events(kb[i], ka[i])
+            ev0[i].record(stream)
+            one_step()
+            ev1[i].record(stream)
+            launches += ctx.last_launch_count() + (1 if world > 1 else 0)
+        ctx.set_profile_events(None, None)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
+    kern_ms = [a.elapsed_time(b) for a, b in zip(kb, ka)]
+    ms = statistics.mean(step_ms)
+    kms = statistics.mean(kern_ms)
+    if world > 1:
+        t = torch.tensor([ms, kms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, kms = float(t[0]), float(t[1])
+    value = world * n / (ms * 1e-3) / 1e9
+
+    # ---- e2e through the host-pointer C-ABI call
+    e2e = None
+    if not args.no_e2e:
+        host = pts.cpu().pin_memory()
+        out_h = torch.empty_like(host).pin_memory()
+        cnt_h = torch.zeros(inst, dtype=torch.int32).pin_memory()
+        e_times = []
+        for i in range(args.warmup + args.steps):
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            rc = H.build_hood_host_ptr(ctx, host.data_ptr(), n, f64, out_h.data_ptr(), cnt_h.data_ptr(), block)
+            if rc:
+                raise RuntimeError(f"host build failed: {rc}")
+            if world > 1:
+                corners[: int(cnt_h[0])].copy_(out_h[: int(cnt_h[0])], non_blocking=True)
+                counts[0] = int(cnt_h[0])
+                exchange()
+                final_cnt.item()
+            if i >= args.warmup:
+                e_times.append(time.perf_counter() - t0)
+        e_ms = statistics.mean(e_times) * 1e3
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t[0])
+        d2h = inst * 4 + int(cnt_h.sum()) * bpp
+        e2e = {"value": world * n / (e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e_ms,
+               "h2d_bytes_per_step": n * bpp, "d2h_bytes_per_step": d2h}
+
+    if rank == 0:
+        peak, peak_src = peaks()
+        achieved = n * bpp / (kms * 1e-3) / 1e9
+        cpu = None
+        if world == 1:
+            hostpts = pts.cpu().numpy()
+            if block:
+                rate, kind, reps = cpu_reference_batched_rate(hostpts, block, args.cpu_seconds, 1)
+            else:
+                rate, kind, reps = cpu_reference_rate(hostpts, args.cpu_seconds, 1)
+            cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": kind,
+                   "sample": f"full workload ({n} points) x {reps} runs (median), "
+                             f"{'oracle/_ref = reference oracle::upper_hull' if kind == 'reference' else 'C port'}"
+                             f", single thread, same input"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": desc, "n_per_rank": n, "storage": storage, "bytes_per_point": bpp,
+                       "block_len": block or n, "l2": "flushed (256 MiB write) between timed steps",
+                       "predicate": "reference double orient, certified f32 filter",
+                       "parallelism": f"x-slab dp{world}" if world > 1 else "single GPU"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(args.config),
+                         "kernel": "slab_hull_kernel", "kernel_ms": kms,
+                         "algorithmic_bytes_per_launch": n * bpp, "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": sampler.summary(),
+            "impl": "ours",
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

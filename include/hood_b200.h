@@ -101,6 +101,11 @@ int hood_last_error(hood_ctx* ctx, hood_error* out);
 /* Number of kernels the last build enqueued (bench bookkeeping). */
 int hood_last_launch_count(hood_ctx* ctx);
 
+/* Optional: record two cudaEvent_t around the slab kernel of every later
+ * device build on its stream (roofline timing of the dominant kernel).
+ * Pass NULLs to stop. */
+int hood_set_profile_events(hood_ctx* ctx, void* ev_before_slab, void* ev_after_slab);
+
 const char* hood_status_string(int status);
 int hood_abi_version(void);
 

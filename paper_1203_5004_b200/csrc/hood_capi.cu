@@ -14,6 +14,8 @@
 #include <cstdint>
 #include <cstring>
 #include <mutex>
+#include <cstdio>
+#include <cstdlib>
 
 #include "../../include/hood_b200.h"
 #include "hood_device.cuh"
@@ -28,6 +30,7 @@ struct hood_ctx {
   int* seg_cnt = nullptr;
   void* seg_ymax = nullptr;  // double-sized slots (fits float too)
   long long* seg_base = nullptr;
+  unsigned* pub = nullptr;
   long long seg_cap = 0;
   DevError* err = nullptr;
   // host-path buffers
@@ -45,6 +48,9 @@ struct hood_ctx {
   bool have_last = false;
   int last_launches = 0;
   int sticky_cuda = 0;
+  cudaEvent_t prof_before = nullptr, prof_after = nullptr;
+  int dbg = 0;
+  long long* trace = nullptr;
 };
 
 namespace {
@@ -70,12 +76,13 @@ struct Plan {
   long long units = 0, tpu = 1;
   int grid = 0;
   int seg_chunks = 256;
+  int rows = 256;       // chunk rows per tile (TMA box height)
+  long long T = 0;      // points per tile
 };
 
 template <class S>
 int make_plan(hood_ctx* ctx, long long n, long long block_len, Plan& pl) {
   constexpr int K = PointT<S>::K;
-  constexpr long long T = (long long)kThreads * K;
   if (n < 1) return HOOD_ERR_INVALID_ARG;
   pl.n = n;
   pl.L = (block_len <= 0 || block_len == n) ? n : block_len;
@@ -83,23 +90,31 @@ int make_plan(hood_ctx* ctx, long long n, long long block_len, Plan& pl) {
     if ((pl.L & (pl.L - 1)) != 0 || n % pl.L != 0 || pl.L < K) return HOOD_ERR_INVALID_ARG;
   }
   pl.instances = n / pl.L;
+  const long long Th = (long long)slab_tile_rows<S>(true) * K;
+  pl.hmode = (pl.L == n || pl.L >= Th);
+  pl.rows = slab_tile_rows<S>(pl.hmode);
+  const long long T = (long long)pl.rows * K;
+  pl.T = T;
   pl.tiles = (n + T - 1) / T;
-  const long long resident = (long long)slab_kernel_occupancy<S>() * ctx->sms;
-  if (pl.L == n || pl.L >= T) {
-    pl.hmode = true;
-    pl.seg_chunks = kThreads;
+  if (pl.hmode) {
+    // one unit (contiguous x-range) per warp of the slab kernel
+    const long long nw = slab_warps_per_cta<S>();
+    const long long ctas = (long long)slab_kernel_occupancy<S>() * ctx->sms;
+    pl.seg_chunks = 32;
     pl.tpi = (pl.L + T - 1) / T;
-    long long spi = resident / pl.instances;
+    long long spi = ctas * nw / pl.instances;
     spi = std::max(1LL, std::min(spi, std::min(pl.tpi, (long long)kMaxSlabsPerInstance)));
     pl.spi = (int)spi;
     pl.units = pl.instances * pl.spi;
+    if (pl.tpi >= (1LL << 31) || pl.units >= (1LL << 31)) return HOOD_ERR_CAPACITY;
+    pl.grid = (int)std::min((pl.units + nw - 1) / nw, ctas);
   } else {
-    pl.hmode = false;
+    const long long resident = (long long)instance_kernel_occupancy<S>() * ctx->sms;
     pl.seg_chunks = (int)(pl.L / K);
     pl.tpu = std::max(1LL, (pl.tiles + resident - 1) / resident);
     pl.units = (pl.tiles + pl.tpu - 1) / pl.tpu;
+    pl.grid = (int)std::min(pl.units, resident);
   }
-  pl.grid = (int)std::min(pl.units, resident);
   return HOOD_OK;
 }
 
@@ -111,10 +126,12 @@ int ensure_ws(hood_ctx* ctx, long long slabs) {
     cudaFree(ctx->seg_cnt);
     cudaFree(ctx->seg_ymax);
     cudaFree(ctx->seg_base);
+    cudaFree(ctx->pub);
     const long long cap = std::max(slabs, 4096LL);
     if (cudaMalloc(&ctx->seg_cnt, cap * sizeof(int)) != cudaSuccess ||
         cudaMalloc(&ctx->seg_ymax, cap * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&ctx->seg_base, cap * sizeof(long long)) != cudaSuccess)
+        cudaMalloc(&ctx->seg_base, cap * sizeof(long long)) != cudaSuccess ||
+        cudaMalloc(&ctx->pub, cap * sizeof(unsigned)) != cudaSuccess)
       return HOOD_ERR_CUDA;
     ctx->seg_cap = cap;
   }
@@ -122,7 +139,7 @@ int ensure_ws(hood_ctx* ctx, long long slabs) {
 }
 
 template <class S>
-int encode_map(const void* pts, long long n, CUtensorMap* map, long long* full_rows) {
+int encode_map(const void* pts, long long n, int box_rows, CUtensorMap* map, long long* full_rows) {
   constexpr int K = PointT<S>::K;
   *full_rows = n / K;
   std::memset(map, 0, sizeof(*map));
@@ -131,7 +148,7 @@ int encode_map(const void* pts, long long n, CUtensorMap* map, long long* full_r
   if (!enc) return HOOD_ERR_CUDA;
   const cuuint64_t gdim[2] = {128, (cuuint64_t)*full_rows};
   const cuuint64_t gstride[1] = {128};
-  const cuuint32_t box[2] = {128, (cuuint32_t)kThreads};
+  const cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(pts), gdim, gstride, box, estr,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -146,6 +163,8 @@ SlabParams<S> slab_params(hood_ctx* ctx, const Plan& pl, const void* pts, void* 
   p.pts = pts;
   p.n = pl.n;
   p.L = pl.L;
+  p.log2L = 0;
+  while ((1LL << p.log2L) < pl.L) ++p.log2L;
   p.hmode = pl.hmode ? 1 : 0;
   p.seg_chunks = pl.seg_chunks;
   p.tiles_per_inst = pl.tpi;
@@ -163,6 +182,10 @@ SlabParams<S> slab_params(hood_ctx* ctx, const Plan& pl, const void* pts, void* 
   p.seg_base = ctx->seg_base;
   p.err = ctx->err;
   p.check_range = (flags & HOOD_FLAG_CHECK_RANGE) ? 1 : 0;
+  p.dbg = ctx->dbg;
+  p.trace = ctx->trace;
+  p.read_lim = pl.n;
+  p.pub = ctx->pub;
   return p;
 }
 
@@ -178,8 +201,19 @@ FinalizeParams<S> finalize_params(hood_ctx* ctx, const Plan& pl, void* corners, 
   f.seg_stride = 0;
   f.slabs_per_inst = pl.spi;
   f.L = pl.L;
-  f.fcap = (int)((128 * 1024) / sizeof(V));
+  f.fcap = (int)((64 * 1024) / sizeof(V));
   return f;
+}
+
+// HOOD_DEBUG_SYNC=1: synchronize after every launch and name the failing one.
+void debug_check(const char* what, cudaStream_t st) {
+  static const bool on = [] {
+    const char* e = std::getenv("HOOD_DEBUG_SYNC");
+    return e && e[0] == '1';
+  }();
+  if (!on) return;
+  const cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) std::fprintf(stderr, "[hood_b200] %s failed: %s\n", what, cudaGetErrorString(e));
 }
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -196,17 +230,23 @@ int build_device(hood_ctx* ctx, const S* pts, long long n, long long block_len, 
   if ((rc = ensure_ws(ctx, pl.units))) return rc;
   CUtensorMap map;
   long long full_rows = 0;
-  if ((rc = encode_map<S>(pts, n, &map, &full_rows))) return rc;
+  std::memset(&map, 0, sizeof(map));  // the stream kernel (hmode) reads with LDG, no tensor map
+  if (!pl.hmode && (rc = encode_map<S>(pts, n, pl.rows, &map, &full_rows))) return rc;
   if (cudaMemsetAsync(ctx->err, 0xff, sizeof(DevError), st) != cudaSuccess) return HOOD_ERR_CUDA;
   const SlabParams<S> p = slab_params<S>(ctx, pl, pts, corners, counts, full_rows, flags);
+  if (ctx->prof_before) cudaEventRecord(ctx->prof_before, st);
   launch_slab_kernel<S>(p, &map, pl.grid, st);
+  debug_check("slab kernel", st);
+  if (ctx->prof_after) cudaEventRecord(ctx->prof_after, st);
   int launches = 1;
   if (pl.hmode && pl.spi > 1) {
     launch_finalize<S>(finalize_params<S>(ctx, pl, corners, counts), (int)pl.instances, st);
+    debug_check("finalize", st);
     ++launches;
   }
   if (padded) {
     launch_pad_fill<S>(padded, corners, counts, n, pl.L, st);
+    debug_check("pad fill", st);
     ++launches;
   }
   const cudaError_t e = cudaGetLastError();
@@ -273,7 +313,6 @@ template <class S>
 int build_host(hood_ctx* ctx, const S* h_pts, long long n, long long block_len, S* h_corners, int* h_counts,
                uint32_t flags) {
   using V = typename PointT<S>::V;
-  constexpr long long T = (long long)kThreads * PointT<S>::K;
   if (!ctx || !h_pts || !h_corners || !h_counts) return HOOD_ERR_INVALID_ARG;
   cudaSetDevice(ctx->device);
   Plan pl;
@@ -285,7 +324,8 @@ int build_host(hood_ctx* ctx, const S* h_pts, long long n, long long block_len, 
   S* d_out = reinterpret_cast<S*>(ctx->d_out);
   CUtensorMap map;
   long long full_rows = 0;
-  if ((rc = encode_map<S>(d_in, n, &map, &full_rows))) return rc;
+  std::memset(&map, 0, sizeof(map));
+  if (!pl.hmode && (rc = encode_map<S>(d_in, n, pl.rows, &map, &full_rows))) return rc;
   cudaStream_t sc = ctx->s_copy, sk = ctx->s_comp;
   cudaMemsetAsync(ctx->err, 0xff, sizeof(DevError), sk);
   SlabParams<S> p = slab_params<S>(ctx, pl, d_in, d_out, ctx->d_counts, full_rows, flags);
@@ -297,16 +337,18 @@ int build_host(hood_ctx* ctx, const S* h_pts, long long n, long long block_len, 
       p0 = 0;
       p1 = n;
     } else {
-      p0 = (u0 * pl.tpi / pl.spi) * T;
-      p1 = (u1 == pl.units) ? n : std::min(n, (u1 * pl.tpi / pl.spi) * T);
+      p0 = (u0 * pl.tpi / pl.spi) * pl.T;
+      p1 = (u1 == pl.units) ? n : std::min(n, (u1 * pl.tpi / pl.spi) * pl.T);
     }
     cudaMemcpyAsync(d_in + 2 * p0, h_pts + 2 * p0, (size_t)(p1 - p0) * sizeof(V), cudaMemcpyHostToDevice, sc);
     cudaEventRecord(ctx->ev[c], sc);
     cudaStreamWaitEvent(sk, ctx->ev[c], 0);
     p.unit_lo = u0;
     p.unit_hi = u1;
+    p.read_lim = p1;
     const long long units_c = u1 - u0;
-    launch_slab_kernel<S>(p, &map, (int)std::min<long long>(units_c, pl.grid), sk);
+    const long long per_cta = pl.hmode ? slab_warps_per_cta<S>() : 1;
+    launch_slab_kernel<S>(p, &map, (int)std::min<long long>((units_c + per_cta - 1) / per_cta, pl.grid), sk);
   }
   if (pl.hmode && pl.spi > 1)
     launch_finalize<S>(finalize_params<S>(ctx, pl, d_out, ctx->d_counts), (int)pl.instances, sk);
@@ -352,7 +394,7 @@ int merge_segments(hood_ctx* ctx, const S* seg_pts, const int* counts, long long
   f.seg_stride = stride;
   f.slabs_per_inst = (int)G;
   f.L = G * stride;
-  f.fcap = (int)((128 * 1024) / sizeof(V));
+  f.fcap = (int)((64 * 1024) / sizeof(V));
   launch_finalize<S>(f, 1, st);
   ctx->last_stream = st;
   ctx->have_last = true;
@@ -387,6 +429,7 @@ int hood_destroy(hood_ctx* c) {
   cudaFree(c->seg_cnt);
   cudaFree(c->seg_ymax);
   cudaFree(c->seg_base);
+  cudaFree(c->pub);
   cudaFree(c->err);
   cudaFree(c->d_in);
   cudaFree(c->d_out);
@@ -449,6 +492,22 @@ int hood_last_error(hood_ctx* ctx, hood_error* out) {
 }
 
 int hood_last_launch_count(hood_ctx* ctx) { return ctx ? ctx->last_launches : 0; }
+
+// Internal profiling hooks (not part of the public header): kernel debug
+// mode and a device buffer of 6*64 int64 for per-tile clock64 stamps of CTA 0.
+extern "C" int hood_internal_set_debug(hood_ctx* ctx, int mode, void* trace) {
+  if (!ctx) return HOOD_ERR_INVALID_ARG;
+  ctx->dbg = mode;
+  ctx->trace = reinterpret_cast<long long*>(trace);
+  return HOOD_OK;
+}
+
+int hood_set_profile_events(hood_ctx* ctx, void* before, void* after) {
+  if (!ctx) return HOOD_ERR_INVALID_ARG;
+  ctx->prof_before = reinterpret_cast<cudaEvent_t>(before);
+  ctx->prof_after = reinterpret_cast<cudaEvent_t>(after);
+  return HOOD_OK;
+}
 
 const char* hood_status_string(int s) {
   switch (s) {

@@ -55,6 +55,10 @@ __device__ __forceinline__ bool above(const double2& a, const double2& b, const 
 // known AND the double evaluation of the reference is correct as well, so the
 // verdict equals the reference's double predicate.  Otherwise fall back to
 // the exact reference operation sequence in double (floats promote exactly).
+static __device__ __noinline__ bool above_slow(float ax, float ay, float bx, float by, float cx, float cy) {
+  return above_d((double)ax, (double)ay, (double)bx, (double)by, (double)cx, (double)cy);
+}
+
 __device__ __forceinline__ bool above(const float2& a, const float2& b, const float2& c) {
   const float t1 = __fmul_rn(__fsub_rn(c.x, a.x), __fsub_rn(b.y, a.y));
   const float t2 = __fmul_rn(__fsub_rn(c.y, a.y), __fsub_rn(b.x, a.x));
@@ -63,7 +67,27 @@ __device__ __forceinline__ bool above(const float2& a, const float2& b, const fl
                                 1.0e-36f);
   if (det > bound) return true;
   if (det < -bound) return false;
-  return above_d((double)a.x, (double)a.y, (double)b.x, (double)b.y, (double)c.x, (double)c.y);
+  return above_slow(a.x, a.y, b.x, b.y, c.x, c.y);  // rare: keep it out of the hot code
+}
+
+// Three-way version (+1 above, -1 below, 0 on the chord) with the same
+// semantics: the sign of the reference's double orient(b, a, c).
+__device__ __forceinline__ int orient_sign_d(double ax, double ay, double bx, double by, double cx, double cy) {
+  const double t1 = __dmul_rn(__dsub_rn(cx, ax), __dsub_rn(by, ay));
+  const double t2 = __dmul_rn(__dsub_rn(cy, ay), __dsub_rn(bx, ax));
+  return (t1 > t2) - (t1 < t2);
+}
+__device__ __forceinline__ int orient_sign(const double2& a, const double2& b, const double2& c) {
+  return orient_sign_d(a.x, a.y, b.x, b.y, c.x, c.y);
+}
+__device__ __forceinline__ int orient_sign(const float2& a, const float2& b, const float2& c) {
+  const float t1 = __fmul_rn(__fsub_rn(c.x, a.x), __fsub_rn(b.y, a.y));
+  const float t2 = __fmul_rn(__fsub_rn(c.y, a.y), __fsub_rn(b.x, a.x));
+  const float det = __fsub_rn(t1, t2);
+  const float bound = __fmaf_rn(4.76837158203125e-07f, __fadd_rn(fabsf(t1), fabsf(t2)), 1.0e-36f);
+  if (det > bound) return 1;
+  if (det < -bound) return -1;
+  return orient_sign_d((double)a.x, (double)a.y, (double)b.x, (double)b.y, (double)c.x, (double)c.y);
 }
 
 // --------------------------------------------------------------- accessors
@@ -129,7 +153,7 @@ __device__ __forceinline__ bool low_f(const AccA& A, i64 as, i64 i, const AccB& 
 }
 
 template <class V, class AccA, class AccB>
-__device__ void bridge(const AccA& A, i64 as, i64 m, const AccB& B, i64 bs, i64 k,
+__device__ __noinline__ void bridge(const AccA& A, i64 as, i64 m, const AccB& B, i64 bs, i64 k,
                        i64& pidx, i64& qidx) {
   // Concatenation test: (m-1, 0) is the bridge iff both classifiers are EQUAL
   // there (the pinpoint phase, kernel.cpp:101-112).  Arc-like inputs stop here.

@@ -2,59 +2,66 @@
 //
 // The reference round loop (driver.cpp:19-45) launches log2(n)-1 merge rounds
 // over REMOTE-padded blocks, each round touching all 36n bytes of hood /
-// newhood / scratch (psim.cpp:40-47).  Here one HBM pass does the work:
+// newhood / scratch (psim.cpp:40-47).  Here one HBM pass does the work.
 //
-//   slab_hull_kernel  (the hot kernel, HBM-bound: reads 8n / 16n bytes once)
-//     persistent CTAs, each owning a contiguous slab of 32 KB tiles streamed
-//     through a 3-stage TMA (cp.async.bulk.tensor, 128B swizzle) + mbarrier
-//     ring.  Per tile: each of 256 threads owns one 128-byte chunk row
-//     (16 float2 / 8 double2 points) and
-//       1. finds its chunk's max y, checks x strictly increasing (fused
-//          validate_points, hoodbuf.cpp:48-58);
-//       2. block scans give every chunk an anchor height
-//          tau = min(max y of all points to its left in the slab,
-//                    max y of all points to its right up to the end of the
-//                    NEXT tile).  A point with y < tau lies strictly below the
-//          chord of two input points that straddle it, so it is not a corner
-//          of the final hood and is dropped with ONE compare (the
-//          reference's low stages do ~2 predicate calls per point per round);
-//       3. runs the monotone chain (oracle.cpp:7-20) over the survivors of its
-//          chunk, the stack living in its own swizzled smem row;
-//       4. merges the 256 chunk hoods with a CTA merge tree (bridge = the
-//          reference's g/f classifiers as monotone searches, splice =
-//          kernel.cpp:117-137 without padding);
-//       5. merges the tile hood into the slab's running hood (smem, spilling
-//          to the output slots in HBM when it outgrows kHCap -- the arc).
-//   finalize_kernel   one CTA per instance: cull slab hoods against the slab
-//     maxima on both sides, then merge the survivors (smem fast path, or in
-//     place in HBM for huge hoods) -- the paper's high stages on compacted
-//     hoods only.
-//   pad_fill_kernel   optional REMOTE-padded n-slot output (HoodBuffer layout,
-//     hoodbuf.cpp:72-92) for drop-in callers that want the padded form.
+// slab_hull_kernel (instances spanning >= 1 tile; the hot kernel, HBM-bound:
+//   it reads the 8n / 16n input bytes exactly once).  Persistent CTAs, 2 per
+//   SM, each owning a contiguous x-slab streamed in 32 KB tiles through a
+//   3-stage TMA ring (cp.async.bulk.tensor, 128B swizzle, mbarrier
+//   complete_tx).  Warp-specialised:
+//     * 8 compute warps, one 128-byte chunk row (16 float2 / 8 double2
+//       points) per thread.  Per tile: max y of its chunk of the NEXT tile
+//       (one tile of lookahead), one named barrier to exchange warp maxima,
+//       then every warp gets an anchor height
+//         tau = min(max y left of the warp in the slab, max y right of it
+//                   up to the end of the next tile).
+//       A point with y < tau lies strictly below the chord between two input
+//       points that straddle it, so it cannot be a corner of the final hood;
+//       one compare drops it.  The rare survivors run the reference monotone
+//       chain (oracle.cpp:7-20) in the thread's own swizzled smem row.  x is
+//       checked strictly increasing on the way (validate_points,
+//       hoodbuf.cpp:48-58).
+//     * 1 merger warp: consumes each tile's chunk hoods (mbarrier `ready`),
+//       folds them into the slab's running hood -- point-by-point chain
+//       pushes when few survive (the common case), a warp merge tree + one
+//       bridge (the reference's g/f classifiers as monotone searches,
+//       kernel.hpp:31-67, splice kernel.cpp:117-137) when many do -- then
+//       releases the stage and issues the next TMA load.
+// instance_hull_kernel (batched instances shorter than a tile): whole
+//   instances per tile, exact per-chunk anchors inside every instance, CTA
+//   merge tree per instance, hood written straight to the output slots.
+// finalize_kernel: one CTA per instance spanning several slabs: cull slab
+//   hoods against the slab maxima on both sides, then hull the survivors
+//   (chain in smem, or a merge tree in place in HBM for huge hoods).
+// pad_fill_kernel: optional REMOTE-padded n-slot output (HoodBuffer layout).
 #include "hood_device.cuh"
 #include "hood_kernels.cuh"
 
 #include <cstdio>
+#include <cstdlib>
 
 namespace hood_b200 {
 
-template <class S> struct HCap { static constexpr int value = 8192 / (int)(2 * sizeof(S)); };
+template <class S> struct HCap { static constexpr int value = 128; };  // running hood kept in smem (corners)
+
+constexpr int kSeqMax = 96;                   // survivors per tile folded point by point
 
 __device__ __forceinline__ unsigned char* align1024(unsigned char* p) {
   const unsigned a = smem_u32(p);
   return p + ((1024u - (a & 1023u)) & 1023u);
 }
 
-template <class S>
-constexpr size_t slab_smem_bytes() {
-  using V = typename PointT<S>::V;
-  return 1024 + (size_t)kStages * kTileBytes + (size_t)HCap<S>::value * sizeof(V) +
-         kThreads * sizeof(long long) + kThreads * sizeof(int) + 64 * sizeof(S) +
-         kStages * sizeof(uint64_t) + 16 * sizeof(long long) + 64;
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int NT>
+__device__ __forceinline__ void compute_barrier() {
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
 }
 
 template <class S>
-__device__ __forceinline__ void load_row(const unsigned char* row_base, int t, typename PointT<S>::V* v);
+__device__ __forceinline__ void load_row(const unsigned char* stage, int t, typename PointT<S>::V* v);
 
 template <>
 __device__ __forceinline__ void load_row<float>(const unsigned char* stage, int t, float2* v) {
@@ -74,36 +81,797 @@ __device__ __forceinline__ void load_row<double>(const unsigned char* stage, int
   for (int u = 0; u < 8; ++u) v[u] = *reinterpret_cast<const double2*>(row + ((u ^ (t & 7)) << 4));
 }
 
+// Own chunk of a tile: smem row when the chunk is full, global otherwise
+// (only the very last chunk of an input can be partial).
 template <class S>
-__device__ __forceinline__ S row_ymax(const unsigned char* stage, int t) {
+__device__ __forceinline__ void load_chunk(const unsigned char* stage, int t, const typename PointT<S>::V* gpts,
+                                           long long base, int nv, typename PointT<S>::V* v) {
+  constexpr int K = PointT<S>::K;
   using V = typename PointT<S>::V;
-  V v[PointT<S>::K];
-  load_row<S>(stage, t, v);
-  S m = v[0].y;
+  if (nv == K) {
+    load_row<S>(stage, t, v);
+  } else {
 #pragma unroll
-  for (int i = 1; i < PointT<S>::K; ++i) m = fmax(m, v[i].y);
+    for (int i = 0; i < K; ++i) v[i] = (i < nv) ? gpts[base + i] : V{};
+  }
+}
+
+template <class S>
+__device__ __forceinline__ S chunk_max(const typename PointT<S>::V* v, int nv) {
+  constexpr int K = PointT<S>::K;
+  S m = neg_inf<S>();
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+    if (i < nv) m = fmax(m, v[i].y);
   return m;
 }
 
-// ------------------------------------------------------------------ slab kernel
+template <class S>
+__device__ __forceinline__ S warp_max(S v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Warp maximum through one REDUX on an order-preserving 32-bit key.  Exact
+// for float; a double is rounded toward -inf first, so the result never
+// exceeds the true maximum (still a valid anchor height).
+__device__ __forceinline__ unsigned okey(float f) {
+  const unsigned b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float okey_inv(unsigned k) {
+  return k == 0u ? -__int_as_float(0x7f800000) : __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+template <class S>
+__device__ __forceinline__ S warp_max_fast(S v) {
+  const float f = sizeof(S) == 4 ? (float)v : __double2float_rd((double)v);
+  return (S)okey_inv(__reduce_max_sync(0xffffffffu, okey(f)));
+}
+
+// x strictly increasing (and optionally inside (0,1)); on failure record
+// the first offending index (key = 2*index + is_order_error).  The slow path
+// re-reads the chunk from global memory so the register copy stays in
+// registers.
+template <class S>
+__device__ __noinline__ void report_bad(const typename PointT<S>::V* gpts, int nv, S prevx, bool has_prev,
+                                        long long base, int check_range, DevError* err) {
+  unsigned long long bad = ~0ULL;
+  S px = prevx;
+  for (int i = 0; i < nv; ++i) {
+    const S x = gpts[base + i].x;
+    if (check_range && !(x > (S)0 && x < (S)1)) {
+      bad = (unsigned long long)(base + i) * 2;
+      break;
+    }
+    if ((i > 0 || has_prev) && !(x > px)) {
+      bad = (unsigned long long)(base + i) * 2 + 1;
+      break;
+    }
+    px = x;
+  }
+  if (bad != ~0ULL) atomicMin(&err->key, bad);
+}
+
+template <class S>
+__device__ __forceinline__ void check_chunk(const typename PointT<S>::V* v, int nv, S prevx, bool has_prev,
+                                            long long base, int check_range, DevError* err,
+                                            const typename PointT<S>::V* gpts) {
+  constexpr int K = PointT<S>::K;
+  bool bad = has_prev && nv > 0 && !(v[0].x > prevx);
+#pragma unroll
+  for (int i = 1; i < K; ++i) bad |= (i < nv) && !(v[i].x > v[i - 1].x);
+  if (check_range) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) bad |= (i < nv) && !(v[i].x > (S)0 && v[i].x < (S)1);
+  }
+  if (bad) report_bad<S>(gpts, nv, prevx, has_prev, base, check_range, err);
+}
+
+// Monotone chain (oracle.cpp:7-20) over the surviving points of one chunk,
+// read from and stacked in the thread's own smem row (the stack slot is never
+// past the point being read, so no unread point is overwritten).  A rolled,
+// out-of-line loop: survivors are rare and the hot loop must stay small.
+template <class S>
+__device__ __noinline__ int chunk_chain(unsigned char* tile, int rb, unsigned mask) {
+  using V = typename PointT<S>::V;
+  const TileAcc<S> X{tile};
+  int sp = 0;
+  V s1 = V{}, s2 = V{};
+  while (mask) {
+    const int i = __ffs(mask) - 1;
+    mask &= mask - 1;
+    const V q = X.ld(rb + i);
+    while (sp >= 2 && !above(s2, s1, q)) {
+      --sp;
+      s1 = s2;
+      if (sp >= 2) s2 = X.ld(rb + sp - 2);
+    }
+    X.st(rb + sp, q);
+    ++sp;
+    s2 = s1;
+    s1 = q;
+  }
+  return sp;
+}
+
+// Warp-level merge tree (lane-parallel pair merges, __syncwarp per level).
+template <class V, class Acc>
+__device__ void warp_tree_merge(const Acc& X, long long* ns, int* nc, int num_nodes, int levels, int lane) {
+  for (int l = 0; l < levels; ++l) {
+    const int half = 1 << l, span = half << 1;
+    for (int a = lane * span; a < num_nodes; a += 32 * span) {
+      const int b = a + half;
+      if (b >= num_nodes || nc[b] == 0) continue;
+      long long s = ns[a], m = nc[a];
+      merge_nodes<V>(X, s, m, ns[b], (long long)nc[b]);
+      ns[a] = s;
+      nc[a] = (int)m;
+    }
+    __syncwarp();
+  }
+}
+
+struct HoodState {
+  long long n;  // corners in the running slab hood
+  int in_smem;  // 1: Hs in shared memory, 0: spilled to the output slots
+};
+
+// Many survivors in one tile (arc-like input or a slab edge): the merger warp
+// merges the chunk hoods with a warp merge tree, then bridges the tile hood
+// into the running slab hood (kernel.hpp:31-67 classifiers as monotone
+// searches, kernel.cpp:117-137 splice), spilling it to HBM when it outgrows
+// the smem buffer.  Out of line: the common path never touches this code.
+template <class S, int NW, int HC>
+__device__ __noinline__ HoodState merge_tile_tree(unsigned char* tile, const int* nc, const unsigned* wm,
+                                                  long long* mns, int* mnc, typename PointT<S>::V* Hs,
+                                                  typename PointT<S>::V* gslab, HoodState h) {
+  using V = typename PointT<S>::V;
+  constexpr int K = PointT<S>::K;
+  constexpr int NT = NW * 32;
+  const int lane = threadIdx.x & 31;
+  const TileAcc<S> X{tile};
+  for (int c = lane; c < NT; c += 32) {
+    mns[c] = (long long)c * K;
+    mnc[c] = ((wm[c >> 5] >> (c & 31)) & 1u) ? nc[c] : 0;
+  }
+  __syncwarp();
+  int levels = 0;
+  while ((1 << levels) < NT) ++levels;
+  warp_tree_merge<V>(X, mns, mnc, NT, levels, lane);
+  const long long qs = mns[0], kq = mnc[0];
+  long long pidx = -1, qidx = 0;
+  if (lane == 0 && h.n > 0) {
+    if (h.in_smem) bridge<V>(PtrAcc<V>{Hs}, 0, h.n, X, qs, kq, pidx, qidx);
+    else bridge<V>(PtrAcc<V>{gslab}, 0, h.n, X, qs, kq, pidx, qidx);
+  }
+  pidx = __shfl_sync(0xffffffffu, pidx, 0);
+  qidx = __shfl_sync(0xffffffffu, qidx, 0);
+  const long long newN = pidx + 1 + kq - qidx;
+  if (h.in_smem && newN > HC) {  // spill the kept prefix to the output slots
+    for (long long e = lane; e <= pidx; e += 32) gslab[e] = Hs[e];
+    h.in_smem = 0;
+  }
+  V* dstp = h.in_smem ? Hs : gslab;
+  for (long long e = lane; e < kq - qidx; e += 32) dstp[pidx + 1 + e] = X.ld(qs + qidx + e);
+  __syncwarp();
+  h.n = newN;
+  return h;
+}
+
+// Few survivors (the common case): one lane pushes them into the running
+// hood Hs[0..h) in x order, monotone-chain style (oracle.cpp:13-17).
+template <class S, int NW>
+__device__ __noinline__ long long fold_survivors(unsigned char* tile, const int* nc, const unsigned* wm,
+                                                 typename PointT<S>::V* Hs, long long h) {
+  using V = typename PointT<S>::V;
+  constexpr int K = PointT<S>::K;
+  const TileAcc<S> X{tile};
+  V h1 = h >= 1 ? Hs[h - 1] : V{}, h2 = h >= 2 ? Hs[h - 2] : V{};
+  for (int j = 0; j < NW; ++j) {
+    unsigned m = wm[j];
+    while (m) {
+      const int c = 32 * j + __ffs(m) - 1;
+      m &= m - 1;
+      const int cnt = nc[c];
+      for (int e = 0; e < cnt; ++e) {
+        const V q = X.ld((long long)c * K + e);
+        while (h >= 2 && !above(h2, h1, q)) {
+          --h;
+          h1 = h2;
+          if (h >= 2) h2 = Hs[h - 2];
+        }
+        Hs[h] = q;
+        ++h;
+        h2 = h1;
+        h1 = q;
+      }
+    }
+  }
+  return h;
+}
+
+// A partial chunk (only the last chunk of an input): copy its points from
+// global memory into the thread's swizzled row so the hot loop can always
+// read rows from smem.
+template <class S>
+__device__ __noinline__ void stage_partial_row(unsigned char* tile, int t, const typename PointT<S>::V* gpts,
+                                               long long base, int nv) {
+  constexpr int K = PointT<S>::K;
+  const TileAcc<S> X{tile};
+  for (int i = 0; i < K; ++i)
+    X.st((long long)t * K + i, i < nv ? gpts[base + i] : typename PointT<S>::V{});
+}
+
+// Range check of one chunk (validate_points' x in (0,1)), only with
+// HOOD_FLAG_CHECK_RANGE.
+template <class S>
+__device__ __noinline__ void range_check_row(unsigned char* tile, int t, int nv, long long base, DevError* err) {
+  constexpr int K = PointT<S>::K;
+  const TileAcc<S> X{tile};
+  for (int i = 0; i < nv; ++i) {
+    const S x = X.ld((long long)t * K + i).x;
+    if (!(x > (S)0 && x < (S)1)) {
+      atomicMin(&err->key, (unsigned long long)(base + i) * 2);
+      return;
+    }
+  }
+}
+
+// Exact per-chunk anchors inside one warp, for a warp with no anchor on one
+// side (the first / last slab of an instance has nothing beyond it).
+template <class S>
+__device__ __noinline__ S edge_tau(S cm, S left, S right) {
+  const int lane = threadIdx.x & 31;
+  const S NEG = neg_inf<S>();
+  S pin = cm, sin = cm;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const S a = __shfl_up_sync(0xffffffffu, pin, o);
+    const S b = __shfl_down_sync(0xffffffffu, sin, o);
+    if (lane >= o) pin = fmax(pin, a);
+    if (lane + o < 32) sin = fmax(sin, b);
+  }
+  S pex = __shfl_up_sync(0xffffffffu, pin, 1);
+  S sex = __shfl_down_sync(0xffffffffu, sin, 1);
+  if (lane == 0) pex = NEG;
+  if (lane == 31) sex = NEG;
+  return fmin(fmax(left, pex), fmax(right, sex));
+}
+
+template <class S>
+__device__ __forceinline__ S tree_max_y(const typename PointT<S>::V* v) {
+  constexpr int K = PointT<S>::K;
+  S m[K / 2];
+#pragma unroll
+  for (int i = 0; i < K / 2; ++i) m[i] = fmax(v[2 * i].y, v[2 * i + 1].y);
+#pragma unroll
+  for (int w = K / 4; w >= 1; w >>= 1)
+#pragma unroll
+    for (int i = 0; i < w; ++i) m[i] = fmax(m[i], m[i + w]);
+  return m[0];
+}
+
+// Tagged tile maxima: {tile index + 1 (high 32 bits), order-preserving key
+// of the max y (low 32 bits)} in one 64-bit word.  Warps fold their maxima in
+// with a shared-memory atomicMax, so a later tile's tag always wins a slot
+// and a reader can tell a current value from a stale one without any
+// synchronisation.  Doubles are rounded toward -inf first, which keeps the
+// value a valid anchor (never above a real point's y).
+__device__ __forceinline__ unsigned orderable(float f) {
+  const unsigned b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float from_orderable(unsigned k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+template <class S>
+__device__ __forceinline__ unsigned long long pack_tagged(long long tile, S m) {
+  const float f = sizeof(S) == 4 ? (float)m : __double2float_rd((double)m);
+  return ((unsigned long long)(unsigned)(tile + 1) << 32) | orderable(f);
+}
+template <class S>
+__device__ __forceinline__ bool tagged_is(unsigned long long w, long long tile, S& val) {
+  val = (S)from_orderable((unsigned)w);
+  return (unsigned)(w >> 32) == (unsigned)(tile + 1);
+}
+
+// ------------------------------------------------------------------ stream kernel
+//
+// The hot kernel.  Every warp is an independent pipeline over its own
+// contiguous x-range of the input (a "unit"), read once with coalesced 16-byte
+// streaming loads (LDG.128, evict-first) into an NB-deep register ring of
+// blocks (U loads per lane; 256 float2 / 128 double2 points per block).  Per
+// block the warp
+//   1. takes the maximum y of the NEXT block (warp reduce) as its right anchor
+//      and the running maximum of the unit's earlier blocks as its left
+//      anchor; a point below min(left, right) lies strictly below the chord of
+//      two input points that straddle it, so it cannot be a corner of the final
+//      hood (oracle.cpp:7-20 would pop it) and is dropped with one compare;
+//   2. checks x strictly increasing (fused validate_points, hoodbuf.cpp:48-58);
+//   3. compacts the rare survivors, in x order, into its smem buffer with two
+//      ballots per row, and folds them into its running hood -- monotone-chain
+//      pushes by one lane when few, a warp merge tree + bridge (the reference's
+//      g/f classifiers as monotone searches, kernel.hpp:31-67) when many.
+// No barriers, no shared input staging, no cross-warp traffic.
+
+template <class S> struct Ld16;
+template <> struct Ld16<float> {
+  using T = float4;  // two float2 points
+  static constexpr int PPL = 2;
+};
+template <> struct Ld16<double> {
+  using T = double2;  // one double2 point
+  static constexpr int PPL = 1;
+};
+
+__device__ __forceinline__ float2 pt_of(const float4& q, int e) {
+  return e == 0 ? make_float2(q.x, q.y) : make_float2(q.z, q.w);
+}
+__device__ __forceinline__ double2 pt_of(const double2& q, int) { return q; }
+__device__ __forceinline__ float4 ld_stream(const float4* p) { return __ldcs(p); }
+__device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
+
+// Per-warp shared memory of the stream kernel (byte offsets; see WarpLayout).
+template <class S, int U>
+struct StreamLayout {
+  using V = typename PointT<S>::V;
+  static constexpr size_t up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+  static constexpr int BP = 32 * U * Ld16<S>::PPL;                      // points per block
+  static constexpr size_t SB = 0;                                       // [BP] block survivors
+  static constexpr size_t HS = SB + (size_t)BP * sizeof(V);             // [HC] running unit hood
+  static constexpr size_t MNS = up(HS + (size_t)HCap<S>::value * sizeof(V), 8);  // [32] tree starts
+  static constexpr size_t MNC = MNS + 32 * 8;                           // [32] tree counts
+  static constexpr size_t BYTES = up(MNC + 32 * 4, 16);
+};
+
+// Monotone chain over a linear run X[s, s+cnt) in place; returns the corner
+// count (oracle.cpp:7-20).
+template <class V>
+__device__ int chain_linear(V* X, int s, int cnt) {
+  int sp = 0;
+  V s1 = V{}, s2 = V{};
+  for (int i = 0; i < cnt; ++i) {
+    const V q = X[s + i];
+    while (sp >= 2 && !above(s2, s1, q)) {
+      --sp;
+      s1 = s2;
+      if (sp >= 2) s2 = X[s + sp - 2];
+    }
+    X[s + sp] = q;
+    ++sp;
+    s2 = s1;
+    s1 = q;
+  }
+  return sp;
+}
+
+// Fold m x-sorted survivors SB[0..m) into the running hood Hs[0..h) by
+// monotone-chain pushes (one lane).
+template <class V>
+__device__ __noinline__ long long fold_linear(const V* SB, int m, V* Hs, long long h) {
+  V h1 = h >= 1 ? Hs[h - 1] : V{}, h2 = h >= 2 ? Hs[h - 2] : V{};
+  for (int i = 0; i < m; ++i) {
+    const V q = SB[i];
+    while (h >= 2 && !above(h2, h1, q)) {
+      --h;
+      h1 = h2;
+      if (h >= 2) h2 = Hs[h - 2];
+    }
+    Hs[h] = q;
+    ++h;
+    h2 = h1;
+    h1 = q;
+  }
+  return h;
+}
+
+// Many survivors (arc-like input, an instance edge): the warp hulls 32 runs
+// of SB in parallel, merges them with a warp merge tree and bridges the block
+// hood into the running hood (spilling it to HBM when it outgrows Hs).
+template <class S, int HC>
+__device__ __noinline__ HoodState merge_block_tree(typename PointT<S>::V* SB, int m, long long* mns, int* mnc,
+                                                   typename PointT<S>::V* Hs, typename PointT<S>::V* gslab,
+                                                   HoodState h) {
+  using V = typename PointT<S>::V;
+  const int lane = threadIdx.x & 31;
+  const int ch = (m + 31) / 32;
+  const int s = min(m, lane * ch), e = min(m, s + ch);
+  const int cnt = chain_linear(SB, s, e - s);
+  mns[lane] = s;
+  mnc[lane] = cnt;
+  __syncwarp();
+  warp_tree_merge<V>(PtrAcc<V>{SB}, mns, mnc, 32, 5, lane);
+  const long long qs = mns[0], kq = mnc[0];
+  long long pidx = -1, qidx = 0;
+  if (lane == 0 && h.n > 0) {
+    if (h.in_smem) bridge<V>(PtrAcc<V>{Hs}, 0, h.n, PtrAcc<V>{SB}, qs, kq, pidx, qidx);
+    else bridge<V>(PtrAcc<V>{gslab}, 0, h.n, PtrAcc<V>{SB}, qs, kq, pidx, qidx);
+  }
+  pidx = __shfl_sync(0xffffffffu, pidx, 0);
+  qidx = __shfl_sync(0xffffffffu, qidx, 0);
+  const long long newN = pidx + 1 + kq - qidx;
+  if (h.in_smem && newN > HC) {  // spill the kept prefix to the output slots
+    for (long long i = lane; i <= pidx; i += 32) gslab[i] = Hs[i];
+    h.in_smem = 0;
+  }
+  V* dstp = h.in_smem ? Hs : gslab;
+  for (long long i = lane; i < kq - qidx; i += 32) dstp[pidx + 1 + i] = SB[qs + qidx + i];
+  __syncwarp();
+  h.n = newN;
+  return h;
+}
+
+// One 16-byte unit of the partial block at the end of an input, reading only
+// the `avail` points that exist; missing points get y = -inf (never survive,
+// never raise an anchor).
+template <class S>
+__device__ __forceinline__ typename Ld16<S>::T partial_load(const typename Ld16<S>::T* src,
+                                                            const typename PointT<S>::V* pt, long long avail);
+template <>
+__device__ __forceinline__ float4 partial_load<float>(const float4* src, const float2* pt, long long avail) {
+  const float NI = neg_inf<float>();
+  if (avail >= 2) return *src;
+  if (avail == 1) {
+    const float2 a = *pt;
+    return make_float4(a.x, a.y, NI, NI);
+  }
+  return make_float4(NI, NI, NI, NI);
+}
+template <>
+__device__ __forceinline__ double2 partial_load<double>(const double2* src, const double2*, long long avail) {
+  const double NI = neg_inf<double>();
+  return avail >= 1 ? *src : make_double2(NI, NI);
+}
+
+template <class S, int U>
+__device__ __forceinline__ S block_ymax(const typename Ld16<S>::T* b) {
+  constexpr int PPL = Ld16<S>::PPL;
+  S m = neg_inf<S>();
+#pragma unroll
+  for (int j = 0; j < U; ++j)
+#pragma unroll
+    for (int e = 0; e < PPL; ++e) m = fmax(m, pt_of(b[j], e).y);
+  return m;
+}
+
+// Slow path of the fused x check: lane-parallel scan of one block for the
+// first point not strictly right of its predecessor (same instance).
+template <class S, int U>
+__device__ __noinline__ void report_bad_block(const typename PointT<S>::V* gpts, long long bs, long long lim,
+                                              long long ibase, DevError* err) {
+  constexpr int BP = 32 * U * Ld16<S>::PPL;
+  const int lane = threadIdx.x & 31;
+  const long long e = min(lim, bs + BP);
+  for (long long q = bs + lane; q < e; q += 32)
+    if (q > ibase && !(gpts[q].x > gpts[q - 1].x)) atomicMin(&err->key, (unsigned long long)q * 2 + 1);
+}
+
+// validate_points' x in (0, 1) (only with HOOD_FLAG_CHECK_RANGE).
+template <class S, int U>
+__device__ __noinline__ void range_check_block(const typename PointT<S>::V* gpts, long long bs, long long lim,
+                                               DevError* err) {
+  constexpr int BP = 32 * U * Ld16<S>::PPL;
+  const int lane = threadIdx.x & 31;
+  const long long e = min(lim, bs + BP);
+  for (long long q = bs + lane; q < e; q += 32) {
+    const S x = gpts[q].x;
+    if (!(x > (S)0 && x < (S)1)) atomicMin(&err->key, (unsigned long long)q * 2);
+  }
+}
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)), "l"(gsrc),
+               "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Per-warp shared memory of the ring kernel.
+template <class S, int D>
+struct RingLayout {
+  using V = typename PointT<S>::V;
+  static constexpr size_t up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+  static constexpr int U = 4;                                           // 16-byte units per lane per block
+  static constexpr int R = D + 2;                                       // ring slots
+  static constexpr int BP = 32 * U * Ld16<S>::PPL;                      // points per block
+  static constexpr size_t BB = 32 * U * 16;                             // bytes per block (2 KB)
+  static constexpr size_t RING = 0;                                     // [R] blocks, lane-interleaved
+  static constexpr size_t BM = RING + (size_t)R * BB;                   // [R] block maxima
+  static constexpr size_t SB = up(BM + (size_t)R * sizeof(S), 16);      // [BP] block survivors
+  static constexpr size_t HS = SB + (size_t)BP * sizeof(V);             // [HC] running unit hood
+  static constexpr size_t MNS = up(HS + (size_t)HCap<S>::value * sizeof(V), 8);  // [32] tree starts
+  static constexpr size_t MNC = MNS + 32 * 8;                           // [32] tree counts
+  static constexpr size_t BYTES = up(MNC + 32 * 4, 128);
+};
+
+// The hot kernel.  Every warp is an independent pipeline over its own
+// contiguous x-range of the input (a "unit").  Its lanes stream the unit's 2 KB
+// blocks (256 float2 / 128 double2 points) with coalesced 16-byte cp.async into
+// a per-warp ring of R = D + 2 smem slots, D blocks ahead of the block being
+// processed.  A block's maximum y is taken when it lands; the block itself is
+// processed D iterations later with
+//   left  = max y of the unit's earlier blocks (or of the EXT points before
+//           the unit),
+//   right = max y of the next D blocks (or of the EXT points after the unit),
+// both sets strictly left / right of every point of the block: a point below
+// min(left, right) lies strictly below the chord of two input points that
+// straddle it, cannot be a corner of the final hood (oracle.cpp:7-20 pops it)
+// and is dropped with one compare.  The rare survivors are compacted in x
+// order with ballots and folded into the warp's running hood (monotone-chain
+// pushes, or a warp merge tree + bridge -- kernel.hpp:31-67 -- when many).
+// x strictly increasing is checked on the way (validate_points,
+// hoodbuf.cpp:48-58).  Lanes only ever read the smem bytes they copied
+// themselves, so no barrier of any kind is needed.
+template <class S, int D>
+__global__ void __launch_bounds__(128) ring_hull_kernel(const SlabParams<S> p) {
+  using V = typename PointT<S>::V;
+  using L = typename Ld16<S>::T;
+  using LY = RingLayout<S, D>;
+  constexpr int U = LY::U, R = LY::R, PPL = Ld16<S>::PPL;
+  constexpr int BP = LY::BP;
+  constexpr int BB = (int)LY::BB;
+  constexpr int HC = HCap<S>::value;
+  constexpr int EXT = 128;
+
+  extern __shared__ unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char* wb = smem_raw + (size_t)warp * LY::BYTES;
+  unsigned char* ring = wb + LY::RING + lane * 16;  // this lane's column of the ring
+  V* SB = reinterpret_cast<V*>(wb + LY::SB);
+  V* Hs = reinterpret_cast<V*>(wb + LY::HS);
+  long long* mns = reinterpret_cast<long long*>(wb + LY::MNS);
+  int* mnc = reinterpret_cast<int*>(wb + LY::MNC);
+  const V* gpts = reinterpret_cast<const V*>(p.pts);
+  const unsigned char* gbytes = reinterpret_cast<const unsigned char*>(p.pts) + lane * 16;
+  V* gout = reinterpret_cast<V*>(p.out);
+  const S NEG = neg_inf<S>();
+  const unsigned below = (1u << lane) - 1u;
+
+  const int spi = p.slabs_per_inst;
+  const long long bpi = p.tiles_per_inst;  // blocks per instance
+  const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
+  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+
+  for (long long u = p.unit_lo + gw; u < p.unit_hi; u += nwarps) {
+    const int uu = (int)u, inst = uu / spi, jslab = uu - inst * spi;
+    const long long b0 = (long long)inst * bpi + ((long long)jslab * bpi) / spi;  // global block indices
+    const long long b1 = (long long)inst * bpi + ((long long)(jslab + 1) * bpi) / spi;
+    const int nblk = (int)(b1 - b0);
+    const long long ibase = (long long)inst * p.L;
+    const long long lim = min(p.n, ibase + p.L);
+    const long long ubase = b0 * BP;
+    const long long uend = min(b1 * BP, lim);
+    const int nfull = (int)min((long long)nblk, (lim - ubase) / BP);  // blocks [0, nfull) are full
+    const long long lim_bytes = lim * (long long)sizeof(V);
+
+    // copy block k of the unit into ring slot s (lane column); full blocks
+    // take four plain 16-byte copies, the input's last block is clamped
+    auto issue = [&](int k, int s) {
+      const long long off = (b0 + k) * (long long)BB;
+      unsigned char* dst = ring + s * BB;
+      if (k < nfull) {
+#pragma unroll
+        for (int j = 0; j < U; ++j) cp_async16(dst + j * 512, gbytes + off + j * 512, 16);
+      } else {
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          const long long rem = lim_bytes - (off + lane * 16 + j * 512);
+          const int nb = rem >= 16 ? 16 : (rem > 0 ? (int)rem : 0);
+          cp_async16(dst + j * 512, nb ? gbytes + off + j * 512 : gbytes, nb);
+        }
+      }
+    };
+    // max y of block k (slot s) over the warp; the partial block masks points
+    auto block_max = [&](int k, int s) -> S {
+      const unsigned char* src = ring + s * BB;
+      S m = NEG;
+      if (k < nfull) {
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          const L c = *reinterpret_cast<const L*>(src + j * 512);
+#pragma unroll
+          for (int e = 0; e < PPL; ++e) m = fmax(m, pt_of(c, e).y);
+        }
+      } else {
+        const long long q0 = ubase + (long long)k * BP + lane * PPL;
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          const L c = *reinterpret_cast<const L*>(src + j * 512);
+#pragma unroll
+          for (int e = 0; e < PPL; ++e)
+            if (q0 + j * 32 * PPL + e < lim) m = fmax(m, pt_of(c, e).y);
+        }
+      }
+      return warp_max_fast(m);
+    };
+
+    // edge anchors: max y of up to EXT points on each side of the unit
+    S ext_l = NEG, ext_r = NEG;
+    {
+      const long long l0 = max(ibase, ubase - EXT);
+      for (long long i = l0 + lane; i < ubase; i += 32) ext_l = fmax(ext_l, gpts[i].y);
+      const long long r1 = min(min(lim, p.read_lim), uend + EXT);
+      for (long long i = uend + lane; i < r1; i += 32) ext_r = fmax(ext_r, gpts[i].y);
+      ext_l = warp_max(ext_l);
+      ext_r = warp_max(ext_r);
+    }
+
+    // prologue: blocks 0 .. D in flight (one commit group each); maxima of
+    // blocks 1 .. D-1 into the window (block D's comes with iteration 0)
+#pragma unroll
+    for (int k = 0; k <= D; ++k) {
+      if (k < nblk) issue(k, k);
+      cp_async_commit();
+    }
+    cp_async_wait<1>();
+    S wcur = block_max(0, 0);  // max y of the block being processed
+    S win[D];                  // win[i] = max y of block k+1+i (NEG past the unit)
+#pragma unroll
+    for (int i = 0; i < D; ++i) win[i] = (i + 1 < D && i + 1 < nblk) ? block_max(i + 1, i + 1) : NEG;
+
+    S runmax = ext_l;          // left anchor: everything before the block
+    S umax = NEG;              // the unit's own points (finalize anchor)
+    S lastx = NEG;             // x of the previous block's last point
+    HoodState hs{0, 1};
+    int s_cur = 0;             // ring slot of block k
+    int s_far = D;             // ring slot of block k + D
+    int s_new = D + 1;         // ring slot of block k + D + 1
+
+#pragma unroll 1
+    for (int k = 0; k < nblk; ++k) {
+      // keep D+1 blocks in flight: issue k+D+1, then block k+D has landed
+      if (k + D + 1 < nblk) issue(k + D + 1, s_new);
+      cp_async_commit();
+      cp_async_wait<1>();
+      const S mfar = (k + D < nblk) ? block_max(k + D, s_far) : NEG;
+      win[D - 1] = mfar;
+      S right = (k + D >= nblk) ? ext_r : NEG;
+#pragma unroll
+      for (int i = 0; i < D; ++i) right = fmax(right, win[i]);
+      const S tau = fmin(runmax, right);
+
+      // the block itself, from this lane's own ring bytes
+      L c[U];
+      {
+        const unsigned char* src = ring + s_cur * BB;
+#pragma unroll
+        for (int j = 0; j < U; ++j) c[j] = *reinterpret_cast<const L*>(src + j * 512);
+      }
+      const long long bs = ubase + (long long)k * BP;
+      const bool full = k < nfull;
+      const bool first_has_prev = k > 0 || ubase > ibase;
+      S prow = lastx;
+      if (k == 0 && ubase > ibase && lane == 0) prow = gpts[ubase - 1].x;
+      bool ok = true, any = false;
+      if (full) {
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          const S x0 = pt_of(c[j], 0).x;
+          const S xl = pt_of(c[j], PPL - 1).x;
+          S px = __shfl_up_sync(0xffffffffu, xl, 1);
+          if (lane == 0) px = (j > 0 || first_has_prev) ? prow : NEG;
+          ok = ok && (x0 > px);
+          if constexpr (PPL == 2) ok = ok && (xl > x0);
+          prow = __shfl_sync(0xffffffffu, xl, 31);
+#pragma unroll
+          for (int e = 0; e < PPL; ++e) any = any || !(pt_of(c[j], e).y < tau);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          const S x0 = pt_of(c[j], 0).x;
+          const S xl = pt_of(c[j], PPL - 1).x;
+          S px = __shfl_up_sync(0xffffffffu, xl, 1);
+          if (lane == 0) px = prow;
+          const long long q0 = bs + (long long)(j * 32 + lane) * PPL;
+          const bool chk = (lane > 0 || j > 0 || first_has_prev) && q0 < lim;
+          ok = ok && (!chk || x0 > px);
+          if constexpr (PPL == 2) ok = ok && (!(q0 + 1 < lim) || xl > x0);
+          prow = __shfl_sync(0xffffffffu, xl, 31);
+#pragma unroll
+          for (int e = 0; e < PPL; ++e) any = any || (!(pt_of(c[j], e).y < tau) && q0 + e < lim);
+        }
+      }
+      if (__any_sync(0xffffffffu, !ok)) report_bad_block<S, U>(gpts, bs, lim, ibase, p.err);
+      lastx = prow;
+      if (p.check_range) range_check_block<S, U>(gpts, bs, lim, p.err);
+
+      if (__any_sync(0xffffffffu, any)) {
+        // compact the survivors into SB in x order (rows j, lanes, elements)
+        int base = 0;
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          bool sv[PPL];
+          unsigned mk[PPL];
+          int before = 0;
+#pragma unroll
+          for (int e = 0; e < PPL; ++e) {
+            const long long q = bs + (long long)(j * 32 + lane) * PPL + e;
+            sv[e] = !(pt_of(c[j], e).y < tau) && (full || q < lim);
+            mk[e] = __ballot_sync(0xffffffffu, sv[e]);
+            before += __popc(mk[e] & below);
+          }
+          int pos = base + before;
+#pragma unroll
+          for (int e = 0; e < PPL; ++e) {
+            if (sv[e]) SB[pos++] = pt_of(c[j], e);
+            base += __popc(mk[e]);
+          }
+        }
+        __syncwarp();
+        if (hs.in_smem && base <= 32 && hs.n + base <= HC) {
+          long long h = hs.n;
+          if (lane == 0) h = fold_linear<V>(SB, base, Hs, h);
+          hs.n = __shfl_sync(0xffffffffu, h, 0);
+        } else {
+          hs = merge_block_tree<S, HC>(SB, base, mns, mnc, Hs, gout + ubase, hs);
+        }
+        __syncwarp();
+      }
+      umax = fmax(umax, wcur);
+      runmax = fmax(runmax, wcur);
+      // slide the window: the block after this one becomes current
+      wcur = win[0];
+#pragma unroll
+      for (int i = 0; i + 1 < D; ++i) win[i] = win[i + 1];
+      s_cur = (s_cur + 1 == R) ? 0 : s_cur + 1;
+      s_far = (s_far + 1 == R) ? 0 : s_far + 1;
+      s_new = (s_new + 1 == R) ? 0 : s_new + 1;
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+
+    if (hs.in_smem)
+      for (long long e = lane; e < hs.n; e += 32) gout[ubase + e] = Hs[e];
+    if (lane == 0) {
+      if (spi == 1) {
+        p.out_counts[inst] = (int)hs.n;
+      } else {
+        p.seg_cnt[u] = (int)hs.n;
+        p.seg_base[u] = ubase;
+        p.seg_ymax[u] = umax;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------ instance kernel
+
+template <class S>
+constexpr size_t inst_smem_bytes() {
+  return 1024 + (size_t)kStages * kTileBytes + kThreads * sizeof(long long) + kThreads * sizeof(int) +
+         64 * sizeof(S) + kStages * sizeof(uint64_t) + 64;
+}
 
 template <class S>
 __global__ void __launch_bounds__(kThreads, 2)
-slab_hull_kernel(const __grid_constant__ CUtensorMap tmap, const SlabParams<S> p) {
+instance_hull_kernel(const __grid_constant__ CUtensorMap tmap, const SlabParams<S> p) {
   using V = typename PointT<S>::V;
   constexpr int K = PointT<S>::K;
   constexpr int T = kThreads * K;
-  constexpr int HC = HCap<S>::value;
 
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = align1024(smem_raw);
   unsigned char* stages = smem;
-  V* Hs = reinterpret_cast<V*>(smem + (size_t)kStages * kTileBytes);
-  long long* ns = reinterpret_cast<long long*>(Hs + HC);
+  long long* ns = reinterpret_cast<long long*>(smem + (size_t)kStages * kTileBytes);
   int* nc = reinterpret_cast<int*>(ns + kThreads);
-  S* red = reinterpret_cast<S*>(nc + kThreads);  // [0,8) seg warp totals, [8,16) next totals
+  S* red = reinterpret_cast<S*>(nc + kThreads);
   uint64_t* bar = reinterpret_cast<uint64_t*>(red + 64);
-  long long* shv = reinterpret_cast<long long*>(bar + kStages);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const V* gpts = reinterpret_cast<const V*>(p.pts);
@@ -116,20 +884,12 @@ slab_hull_kernel(const __grid_constant__ CUtensorMap tmap, const SlabParams<S> p
   }
   __syncthreads();
 
-  auto unit_range = [&](long long u, long long& t0, long long& t1) {
-    if (p.hmode) {
-      const long long inst = u / p.slabs_per_inst, j = u % p.slabs_per_inst;
-      t0 = inst * p.tiles_per_inst + (j * p.tiles_per_inst) / p.slabs_per_inst;
-      t1 = inst * p.tiles_per_inst + ((j + 1) * p.tiles_per_inst) / p.slabs_per_inst;
-    } else {
-      t0 = u * p.tiles_per_unit;
-      t1 = min(t0 + p.tiles_per_unit, p.num_tiles);
-    }
-  };
-
-  // Producer cursor (thread 0 only) -- issues tiles in consumption order.
   long long pu = p.unit_lo + blockIdx.x, pt = 0, pt_end = 0;
   int k_issued = 0;
+  auto unit_range = [&](long long u, long long& t0, long long& t1) {
+    t0 = u * p.tiles_per_unit;
+    t1 = min(t0 + p.tiles_per_unit, p.num_tiles);
+  };
   if (pu < p.unit_hi) unit_range(pu, pt, pt_end);
   auto produce = [&]() {
     if (pu >= p.unit_hi) return;
@@ -149,11 +909,6 @@ slab_hull_kernel(const __grid_constant__ CUtensorMap tmap, const SlabParams<S> p
   if (tid == 0)
     for (int s = 0; s < kStages; ++s) produce();
 
-  // Running slab hood state (block-uniform).
-  long long hN = 0;
-  int hsm = 1;
-  S runmax = NEG;
-
   const int seg = p.seg_chunks;
   const int W = seg < 32 ? seg : 32;
   int levels = 0;
@@ -163,59 +918,24 @@ slab_hull_kernel(const __grid_constant__ CUtensorMap tmap, const SlabParams<S> p
   for (long long u = p.unit_lo + blockIdx.x; u < p.unit_hi; u += gridDim.x) {
     long long t0, t1;
     unit_range(u, t0, t1);
-    const long long slab_base = t0 * T;
-    const long long inst_u = p.hmode ? u / p.slabs_per_inst : 0;
-    const long long lim_h = p.hmode ? min(p.n, (inst_u + 1) * p.L) : p.n;
-
     for (long long g = t0; g < t1; ++g, ++k) {
       const int st = k % kStages;
       unsigned char* tile = stages + (size_t)st * kTileBytes;
       const TileAcc<S> X{tile};
-      const bool has_next = p.hmode && (g + 1 < t1);
       mbar_wait(&bar[st], (unsigned)((k / kStages) & 1));
 
-      // ---- 1. own chunk: load, max y, x order (+ range) check
       const long long base_pt = g * T + (long long)tid * K;
-      const long long lim = p.hmode ? lim_h : p.n;
-      const int nv = (int)max(0LL, min((long long)K, lim - base_pt));
+      const int nv = (int)max(0LL, min((long long)K, p.n - base_pt));
       V v[K];
-      if (nv == K) {
-        load_row<S>(tile, tid, v);
-      } else {
-#pragma unroll
-        for (int i = 0; i < K; ++i) v[i] = (i < nv) ? gpts[base_pt + i] : V{};
-      }
-      S cm = NEG;
-#pragma unroll
-      for (int i = 0; i < K; ++i)
-        if (i < nv) cm = fmax(cm, v[i].y);
+      load_chunk<S>(tile, tid, gpts, base_pt, nv, v);
+      const S cm = chunk_max<S>(v, nv);
       if (nv > 0) {
-        unsigned long long bad = ~0ULL;
-        const bool inst_start = (base_pt % p.L) == 0;
-        if (!inst_start) {
-          const V prev = (tid > 0) ? X.ld((long long)tid * K - 1) : gpts[base_pt - 1];
-          if (!(v[0].x > prev.x)) bad = (unsigned long long)base_pt * 2 + 1;
-        }
-#pragma unroll
-        for (int i = K - 1; i >= 1; --i)
-          if (i < nv && !(v[i].x > v[i - 1].x)) bad = min(bad, (unsigned long long)(base_pt + i) * 2 + 1);
-        if (p.check_range) {
-#pragma unroll
-          for (int i = K - 1; i >= 0; --i)
-            if (i < nv && !(v[i].x > (S)0 && v[i].x < (S)1))
-              bad = min(bad, (unsigned long long)(base_pt + i) * 2);
-        }
-        if (bad != ~0ULL) atomicMin(&p.err->key, bad);
-      }
-      S nx = NEG;
-      if (has_next) {
-        const int st2 = (k + 1) % kStages;
-        mbar_wait(&bar[st2], (unsigned)(((k + 1) / kStages) & 1));
-        const long long nbase = (g + 1) * T + (long long)tid * K;
-        if (nbase + K <= lim) nx = row_ymax<S>(stages + (size_t)st2 * kTileBytes, tid);
+        const bool inst_start = (base_pt & (p.L - 1)) == 0;  // L is a power of two here
+        const S prevx = inst_start ? (S)0 : X.ld((long long)tid * K - 1).x;
+        check_chunk<S>(v, nv, prevx, !inst_start, base_pt, p.check_range, p.err, gpts);
       }
 
-      // ---- 2. anchor heights: segmented exclusive prefix / suffix max
+      // exact segmented exclusive prefix / suffix max of chunk maxima
       const int gl = lane & (W - 1);
       S pin = cm, sin = cm;
 #pragma unroll
@@ -231,107 +951,43 @@ slab_hull_kernel(const __grid_constant__ CUtensorMap tmap, const SlabParams<S> p
       S sex = __shfl_down_sync(0xffffffffu, sin, 1, W);
       if (gl == 0) pex = NEG;
       if (gl == W - 1) sex = NEG;
-      S segmax = __shfl_sync(0xffffffffu, pin, (lane & ~(W - 1)) + W - 1);
-      S nred = nx;
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) nred = fmax(nred, __shfl_xor_sync(0xffffffffu, nred, o));
       if (lane == 31) red[warp] = pin;
-      if (lane == 0) red[8 + warp] = nred;
       __syncthreads();
-      S nextmax = NEG;
-      if (p.hmode) {
-#pragma unroll
-        for (int w = 0; w < 8; ++w) nextmax = fmax(nextmax, red[8 + w]);
-      }
       if (seg > 32) {
         const int nsw = seg >> 5;
         const int sw0 = (warp / nsw) * nsw;
-        S wp = NEG, ws = NEG, wt = NEG;
         for (int w = sw0; w < sw0 + nsw; ++w) {
           const S r = red[w];
-          if (w < warp) wp = fmax(wp, r);
-          if (w > warp) ws = fmax(ws, r);
-          wt = fmax(wt, r);
+          if (w < warp) pex = fmax(pex, r);
+          if (w > warp) sex = fmax(sex, r);
         }
-        pex = fmax(pex, wp);
-        sex = fmax(sex, ws);
-        segmax = wt;
-      }
-      if (p.hmode) {
-        pex = fmax(pex, runmax);
-        sex = fmax(sex, nextmax);
       }
       const S tau = fmin(pex, sex);
 
-      // ---- 3. monotone chain over the survivors (oracle.cpp:7-20)
+      unsigned mask = 0;
+#pragma unroll
+      for (int i = 0; i < K; ++i)
+        if (i < nv && !(v[i].y < tau)) mask |= 1u << i;
       const long long rb = (long long)tid * K;
       int sp = 0;
-      V s1 = V{}, s2 = V{};
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        if (i < nv && !(v[i].y < tau)) {
-          const V q = v[i];
-          while (sp >= 2 && !above(s2, s1, q)) {
-            --sp;
-            s1 = s2;
-            if (sp >= 2) s2 = X.ld(rb + sp - 2);
-          }
-          X.st(rb + sp, q);
-          ++sp;
-          s2 = s1;
-          s1 = q;
-        }
+      if (mask) {
+        if (nv < K)
+          for (int i = 0; i < nv; ++i) X.st(rb + i, v[i]);
+        sp = chunk_chain<S>(tile, (int)rb, mask);
       }
       ns[tid] = rb;
       nc[tid] = sp;
       __syncthreads();
 
-      // ---- 4. CTA merge tree over the chunk hoods of each segment
       tree_merge<V>(X, ns, nc, kThreads, levels);
 
-      if (p.hmode) {
-        // ---- 5. merge the tile hood into the running slab hood
-        if (tid == 0) {
-          const long long qs = ns[0], kq = nc[0];
-          long long pidx = -1, qidx = 0, newN = hN;
-          if (kq > 0) {
-            if (hN > 0) {
-              if (hsm) bridge<V>(PtrAcc<V>{Hs}, 0, hN, X, qs, kq, pidx, qidx);
-              else bridge<V>(PtrAcc<V>{gout + slab_base}, 0, hN, X, qs, kq, pidx, qidx);
-            }
-            newN = pidx + 1 + kq - qidx;
-          } else {
-            pidx = hN - 1;
-            qidx = 0;
-          }
-          shv[0] = pidx;
-          shv[1] = qidx;
-          shv[2] = newN;
-          shv[3] = qs;
-          shv[4] = kq;
-        }
-        __syncthreads();
-        const long long pidx = shv[0], qidx = shv[1], newN = shv[2], qs = shv[3], kq = shv[4];
-        if (kq > 0) {
-          if (hsm && newN > HC) {  // spill the kept prefix to the output slots
-            for (long long e = tid; e <= pidx; e += kThreads) gout[slab_base + e] = Hs[e];
-            hsm = 0;
-          }
-          V* dstp = hsm ? Hs : gout + slab_base;
-          for (long long e = tid; e < kq - qidx; e += kThreads) dstp[pidx + 1 + e] = X.ld(qs + qidx + e);
-          hN = newN;
-        }
-        runmax = fmax(runmax, segmax);
-      } else {
-        // instance mode: every segment root is a finished instance hood
-        const int s0 = (tid / seg) * seg;
-        const long long inst_pt = g * T + (long long)s0 * K;
-        if (inst_pt < p.n) {
-          const long long start = ns[s0];
-          const int cnt = nc[s0];
-          for (int e = tid - s0; e < cnt; e += seg) gout[inst_pt + e] = X.ld(start + e);
-          if (tid == s0) p.out_counts[inst_pt / p.L] = cnt;
-        }
+      const int s0 = (tid / seg) * seg;
+      const long long inst_pt = g * T + (long long)s0 * K;
+      if (inst_pt < p.n) {
+        const long long start = ns[s0];
+        const int cnt = nc[s0];
+        for (int e = tid - s0; e < cnt; e += seg) gout[inst_pt + e] = X.ld(start + e);
+        if (tid == s0) p.out_counts[inst_pt >> p.log2L] = cnt;
       }
       __syncthreads();
       if (tid == 0) {
@@ -339,151 +995,282 @@ slab_hull_kernel(const __grid_constant__ CUtensorMap tmap, const SlabParams<S> p
         produce();
       }
     }
-
-    if (p.hmode) {
-      if (hsm)
-        for (long long e = tid; e < hN; e += kThreads) gout[slab_base + e] = Hs[e];
-      if (tid == 0) {
-        if (p.slabs_per_inst == 1) {
-          p.out_counts[inst_u] = (int)hN;
-        } else {
-          p.seg_cnt[u] = (int)hN;
-          p.seg_ymax[u] = runmax;
-          p.seg_base[u] = slab_base;
-        }
-      }
-      hN = 0;
-      hsm = 1;
-      runmax = NEG;
-      __syncthreads();
-    }
   }
 }
 
 // ------------------------------------------------------------------ finalize
 
+// Block-wide exclusive scans over one value per thread (blockDim = 256).
+template <class T, class Op>
+__device__ __forceinline__ T block_excl_scan(T v, T ident, Op op, T* sh, bool reverse) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T a = reverse ? __shfl_down_sync(0xffffffffu, inc, o) : __shfl_up_sync(0xffffffffu, inc, o);
+    if (reverse ? (lane + o < 32) : (lane >= o)) inc = op(inc, a);
+  }
+  T exc = reverse ? __shfl_down_sync(0xffffffffu, inc, 1) : __shfl_up_sync(0xffffffffu, inc, 1);
+  if (reverse ? lane == 31 : lane == 0) exc = ident;
+  if (reverse ? lane == 0 : lane == 31) sh[warp] = inc;
+  __syncthreads();
+  T carry = ident;
+  for (int w = 0; w < 8; ++w)
+    if (reverse ? (w > warp) : (w < warp)) carry = op(carry, sh[w]);
+  __syncthreads();
+  return op(carry, exc);
+}
+
 template <class S>
 __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams<S> p) {
   using V = typename PointT<S>::V;
   extern __shared__ unsigned char smem_raw[];
+  constexpr int R = kMaxSlabsPerInstance / 256;  // segments per thread (at most)
+  constexpr int MAXC = 256;                      // culling candidates handled in smem
   const int M = p.slabs_per_inst;
   const long long s0 = (long long)blockIdx.x * M;
   const long long ibase = (long long)blockIdx.x * p.L;
   V* gout = reinterpret_cast<V*>(p.out);
   const S NEG = neg_inf<S>();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  long long* base = reinterpret_cast<long long*>(smem_raw);
-  long long* nsd = base + M;
-  S* pre = reinterpret_cast<S*>(nsd + M);
-  S* suf = pre + M;
-  int* cnt = reinterpret_cast<int*>(suf + M);
-  int* lo = cnt + M;
-  int* ncd = lo + M;
-  int* scal = ncd + M;  // [0] total alive
-  V* F = reinterpret_cast<V*>(smem_raw + (((size_t)(reinterpret_cast<unsigned char*>(scal + 8) - smem_raw) + 15) & ~(size_t)15));
+  long long* nsd = reinterpret_cast<long long*>(smem_raw);  // [M] tree path
+  int* ncd = reinterpret_cast<int*>(nsd + M);               // [M]
+  S* shS = reinterpret_cast<S*>((reinterpret_cast<uintptr_t>(ncd + M) + 15) & ~(uintptr_t)15);  // [8]
+  int* shI = reinterpret_cast<int*>(shS + 8);               // [16]
+  long long* cb = reinterpret_cast<long long*>((reinterpret_cast<uintptr_t>(shI + 16) + 7) & ~(uintptr_t)7);  // [MAXC] base
+  int* cc = reinterpret_cast<int*>(cb + MAXC);              // [MAXC] count
+  S* ct = reinterpret_cast<S*>((reinterpret_cast<uintptr_t>(cc + MAXC) + 15) & ~(uintptr_t)15);  // [MAXC] tau
+  int* clo = reinterpret_cast<int*>(ct + MAXC);             // [MAXC] alive start
+  int* cn = clo + MAXC;                                     // [MAXC] alive count
+  int* coff = cn + MAXC;                                    // [MAXC] offset in F
+  V* F = reinterpret_cast<V*>((reinterpret_cast<uintptr_t>(coff + MAXC) + 15) & ~(uintptr_t)15);
 
-  const int tid = threadIdx.x;
-  if (tid == 0) scal[0] = 0;
-  for (int s = tid; s < M; s += blockDim.x) {
-    base[s] = p.seg_base ? p.seg_base[s0 + s] : ibase + (long long)s * p.seg_stride;
-    cnt[s] = p.seg_cnt[s0 + s];
-    S y = NEG;
-    if (p.seg_ymax) y = p.seg_ymax[s0 + s];
-    else
-      for (int e = 0; e < cnt[s]; ++e) y = fmax(y, gout[base[s] + e].y);
-    pre[s] = y;
-    suf[s] = y;
-  }
-  __syncthreads();
-  // inclusive prefix / suffix max (Hillis-Steele; M <= kMaxSlabsPerInstance)
-  for (int o = 1; o < M; o <<= 1) {
-    S a[4], b[4];
-    int c = 0;
-    for (int s = tid; s < M; s += blockDim.x, ++c) {
-      a[c] = (s >= o) ? fmax(pre[s], pre[s - o]) : pre[s];
-      b[c] = (s + o < M) ? fmax(suf[s], suf[s + o]) : suf[s];
-    }
-    __syncthreads();
-    c = 0;
-    for (int s = tid; s < M; s += blockDim.x, ++c) {
-      pre[s] = a[c];
-      suf[s] = b[c];
-    }
-    __syncthreads();
-  }
-  // alive range of every slab hood: corners with y >= tau form one run
-  // (y is unimodal along an upper hull).
-  for (int s = tid; s < M; s += blockDim.x) {
-    const S tau = fmin(s > 0 ? pre[s - 1] : NEG, s + 1 < M ? suf[s + 1] : NEG);
-    const int c = cnt[s];
-    const V* h = gout + base[s];
-    int l = 0, r = c;  // alive [l, r)
-    if (c > 0 && !(h[0].y >= tau && h[c - 1].y >= tau)) {
-      // peak: first i with !(y[i+1] > y[i])
-      int a = 0, b = c - 1;
-      while (a < b) {
-        const int mid = (a + b) >> 1;
-        if (h[mid + 1].y > h[mid].y) a = mid + 1;
-        else b = mid;
-      }
-      const int pk = a;
-      if (!(h[pk].y >= tau)) {
-        l = r = 0;
+  // 1. thread t owns the consecutive segments [t*per, t*per + per)
+  const int per = (M + 255) / 256;
+  long long sb[R];
+  int sc[R];
+  S sy[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const int s = tid * per + j;
+    sb[j] = 0;
+    sc[j] = 0;
+    sy[j] = NEG;
+    if (j < per && s < M) {
+      sb[j] = p.seg_base ? p.seg_base[s0 + s] : ibase + (long long)s * p.seg_stride;
+      sc[j] = p.seg_cnt[s0 + s];
+      if (p.seg_ymax) {
+        sy[j] = p.seg_ymax[s0 + s];
       } else {
-        int x0 = 0, x1 = pk;  // first index in [0,pk] with y >= tau
-        while (x0 < x1) {
-          const int mid = (x0 + x1) >> 1;
-          if (h[mid].y >= tau) x1 = mid;
-          else x0 = mid + 1;
-        }
-        l = x0;
-        int y0 = pk, y1 = c - 1;  // last index in [pk, c) with y >= tau
-        while (y0 < y1) {
-          const int mid = (y0 + y1 + 1) >> 1;
-          if (h[mid].y >= tau) y0 = mid;
-          else y1 = mid - 1;
-        }
-        r = y0 + 1;
+        for (int e = 0; e < sc[j]; ++e) sy[j] = fmax(sy[j], gout[sb[j] + e].y);
       }
     }
-    lo[s] = l;
-    ncd[s] = r - l;
-    atomicAdd(&scal[0], r - l);
+  }
+  S tmax = NEG;
+#pragma unroll
+  for (int j = 0; j < R; ++j) tmax = fmax(tmax, sy[j]);
+  auto mx = [](S a, S b) { return fmax(a, b); };
+  const S pre_t = block_excl_scan<S>(tmax, NEG, mx, shS, false);
+  const S suf_t = block_excl_scan<S>(tmax, NEG, mx, shS, true);
+
+  // 2. anchor height of every segment: its corners below tau lie under the
+  //    chord between the maxima of a segment on each side; segments whose own
+  //    maximum is below tau vanish without a single corner read.  Survivors
+  //    ("candidates") are compacted in x order.
+  bool cand[R];
+  S tauj[R];
+  int ncand = 0;
+  {
+    S pre = pre_t;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      S suf = suf_t;
+#pragma unroll
+      for (int jj = j + 1; jj < R; ++jj) suf = fmax(suf, sy[jj]);
+      tauj[j] = fmin(pre, suf);
+      pre = fmax(pre, sy[j]);
+      cand[j] = sc[j] > 0 && !(sy[j] < tauj[j]);
+      ncand += cand[j];
+    }
+  }
+  auto add = [](int a, int b) { return a + b; };
+  int coff0 = block_excl_scan<int>(ncand, 0, add, shI, false);
+  if (tid == 255) shI[8] = coff0 + ncand;
+  __syncthreads();
+  const int C = shI[8];
+  __syncthreads();
+  const bool small = C <= MAXC;
+  if (small) {
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+      if (cand[j]) {
+        cb[coff0] = sb[j];
+        cc[coff0] = sc[j];
+        ct[coff0] = tauj[j];
+        ++coff0;
+      }
   }
   __syncthreads();
-  const int total = scal[0];
+
+  if (small) {
+    // 3. one warp per candidate: coalesced corner loads, alive run = the
+    //    corners with y >= tau (contiguous: y is unimodal along a hood)
+    for (int c = warp; c < C; c += 8) {
+      const long long b = cb[c];
+      const int cnt = cc[c];
+      const S tau = ct[c];
+      int first = 0x7fffffff, last = -1;
+      for (int e = lane; e < cnt; e += 32)
+        if (!(gout[b + e].y < tau)) {
+          first = min(first, e);
+          last = max(last, e);
+        }
+      first = __reduce_min_sync(0xffffffffu, first);
+      last = __reduce_max_sync(0xffffffffu, last);
+      if (lane == 0) {
+        clo[c] = last >= 0 ? first : 0;
+        cn[c] = last >= 0 ? last - first + 1 : 0;
+      }
+    }
+    __syncthreads();
+    // 4. offsets of the alive runs (x order) and their total
+    const int mine = tid < C ? cn[tid] : 0;
+    int off = 0;
+    {
+      int acc = 0;
+      for (int base = 0; base < C; base += 256) {
+        const int v = (base + tid < C) ? cn[base + tid] : 0;
+        const int o = block_excl_scan<int>(v, 0, add, shI, false);
+        if (base + tid < C) coff[base + tid] = acc + o;
+        if (tid == 255) shI[9] = o + v;
+        __syncthreads();
+        acc += shI[9];
+        __syncthreads();
+      }
+      off = acc;  // total alive corners (uniform)
+      (void)mine;
+    }
+    const int A = off;
+    if (A <= p.fcap) {
+      for (int c = warp; c < C; c += 8)
+        for (int e = lane; e < cn[c]; e += 32) F[coff[c] + e] = gout[cb[c] + clo[c] + e];
+      __syncthreads();
+      // 5. exact strict hull of the A x-sorted survivors.  Point i is a corner
+      //    iff it lies strictly above the chord (a*, b*) joining the point of
+      //    minimal slope to it from the left and of maximal slope from it to
+      //    the right (all canonical predicates); the end points always are.
+      int* flag = reinterpret_cast<int*>(F + A);
+      if (A <= 1024) {
+        for (int i = tid; i < A; i += 256) {
+          int keep = 1;
+          if (i > 0 && i + 1 < A) {
+            const V q = F[i];
+            int as = 0;
+            for (int a = 1; a < i; ++a)
+              if (above(F[as], F[a], q)) as = a;  // slope(a, i) < slope(as, i)
+            int bs = i + 1;
+            for (int b = i + 2; b < A; ++b)
+              if (orient_sign(q, F[bs], F[b]) < 0) bs = b;  // slope(i, b) > slope(i, bs)
+            keep = above(F[as], q, F[bs]) ? 1 : 0;
+          }
+          flag[i] = keep;
+        }
+        __syncthreads();
+        // compact the corners in order
+        int w = 0;
+        {
+          int acc = 0;
+          for (int base = 0; base < A; base += 256) {
+            const int v = (base + tid < A) ? flag[base + tid] : 0;
+            const int o = block_excl_scan<int>(v, 0, add, shI, false);
+            if (base + tid < A && v) gout[ibase + acc + o] = F[base + tid];
+            if (tid == 255) shI[10] = o + v;
+            __syncthreads();
+            acc += shI[10];
+            __syncthreads();
+          }
+          w = acc;
+        }
+        if (tid == 0) p.out_counts[blockIdx.x] = w;
+      } else {
+        // larger: one monotone chain (oracle.cpp:7-20) in place
+        if (tid == 0) {
+          int h = 0;
+          V h1 = V{}, h2 = V{};
+          for (int i = 0; i < A; ++i) {
+            const V q = F[i];
+            while (h >= 2 && !above(h2, h1, q)) {
+              --h;
+              h1 = h2;
+              if (h >= 2) h2 = F[h - 2];
+            }
+            F[h] = q;
+            ++h;
+            h2 = h1;
+            h1 = q;
+          }
+          shI[11] = h;
+        }
+        __syncthreads();
+        const int hc = shI[11];
+        for (int e = tid; e < hc; e += blockDim.x) gout[ibase + e] = F[e];
+        if (tid == 0) p.out_counts[blockIdx.x] = hc;
+      }
+      return;
+    }
+  }
+
+  // huge hoods (the arc, many candidates): merge tree over the slab hoods in
+  // place in HBM, each slab's alive run found with the unimodal y searches
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const int s = tid * per + j;
+    if (j < per && s < M) {
+      int l = 0, r = 0;
+      const int c = sc[j];
+      const S tau = tauj[j];
+      const V* h = gout + sb[j];
+      if (c > 0 && !(sy[j] < tau)) {
+        r = c;
+        if (!(h[0].y >= tau && h[c - 1].y >= tau)) {
+          int a = 0, bq = c - 1;
+          while (a < bq) {
+            const int mid = (a + bq) >> 1;
+            if (h[mid + 1].y > h[mid].y) a = mid + 1;
+            else bq = mid;
+          }
+          const int pk = a;
+          int x0 = 0, x1 = pk;
+          while (x0 < x1) {
+            const int mid = (x0 + x1) >> 1;
+            if (h[mid].y >= tau) x1 = mid;
+            else x0 = mid + 1;
+          }
+          l = x0;
+          int y0 = pk, y1 = c - 1;
+          while (y0 < y1) {
+            const int mid = (y0 + y1 + 1) >> 1;
+            if (h[mid].y >= tau) y0 = mid;
+            else y1 = mid - 1;
+          }
+          r = y0 + 1;
+        }
+      }
+      nsd[s] = sb[j] + l;
+      ncd[s] = r - l;
+    }
+  }
+  __syncthreads();
   int levels = 0;
   while ((1 << levels) < M) ++levels;
-  if (total <= p.fcap) {
-    // fast path: compact the survivors into smem (exclusive scan, thread 0;
-    // M is at most a few thousand)
-    if (tid == 0) {
-      long long off = 0;
-      for (int s = 0; s < M; ++s) {
-        nsd[s] = off;
-        off += ncd[s];
-      }
-    }
-    __syncthreads();
-    for (int s = tid; s < M; s += blockDim.x)
-      for (int e = 0; e < ncd[s]; ++e) F[nsd[s] + e] = gout[base[s] + lo[s] + e];
-    __syncthreads();
-    tree_merge<V>(PtrAcc<V>{F}, nsd, ncd, M, levels);
+  tree_merge<V>(PtrAcc<V>{gout}, nsd, ncd, M, levels);
+  if (tid == 0) {
     const long long st = nsd[0];
     const int hc = ncd[0];
-    for (int e = tid; e < hc; e += blockDim.x) gout[ibase + e] = F[st + e];
-    if (tid == 0) p.out_counts[blockIdx.x] = hc;
-  } else {
-    for (int s = tid; s < M; s += blockDim.x) nsd[s] = base[s] + lo[s];
-    __syncthreads();
-    tree_merge<V>(PtrAcc<V>{gout}, nsd, ncd, M, levels);
-    if (tid == 0) {
-      const long long st = nsd[0];
-      const int hc = ncd[0];
-      if (st != ibase)
-        for (int e = 0; e < hc; ++e) gout[ibase + e] = gout[st + e];
-      p.out_counts[blockIdx.x] = hc;
-    }
+    if (st != ibase)
+      for (int e = 0; e < hc; ++e) gout[ibase + e] = gout[st + e];
+    p.out_counts[blockIdx.x] = hc;
   }
 }
 
@@ -503,19 +1290,64 @@ __global__ void pad_fill_kernel(typename PointT<S>::V* padded, const typename Po
 
 // ------------------------------------------------------------------ host side
 
+// Ring kernel lookahead depth D (blocks of 2 KB per warp); selected once per
+// process (HOOD_RING_D=<D> overrides it for experiments).
+static int ring_depth() {
+  static int d = [] {
+    int v = 4;
+    if (const char* e = std::getenv("HOOD_RING_D")) v = std::atoi(e);
+    return (v == 4 || v == 6 || v == 8 || v == 12) ? v : 4;
+  }();
+  return d;
+}
+
+template <class S, int D>
+static size_t ring_smem() {
+  return (size_t)4 * RingLayout<S, D>::BYTES;
+}
+
+template <class S, int D>
+static int ring_occ_of() {
+  const size_t smem = ring_smem<S, D>();
+  cudaFuncSetAttribute(ring_hull_kernel<S, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int o = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ring_hull_kernel<S, D>, 128, smem);
+  return o > 0 ? o : 1;
+}
+
 template <class S>
-size_t slab_kernel_smem() {
-  return slab_smem_bytes<S>();
+int slab_tile_rows(bool hmode) {
+  // hmode: points per 2 KB block, in 128-byte chunk rows of K points
+  return hmode ? (RingLayout<S, 6>::BP / PointT<S>::K) : kThreads;
+}
+
+template <class S>
+int slab_warps_per_cta() {
+  return 4;
 }
 
 template <class S>
 int slab_kernel_occupancy() {
   static int occ = -1;
   if (occ < 0) {
-    cudaFuncSetAttribute(slab_hull_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)slab_smem_bytes<S>());
+    switch (ring_depth()) {
+      case 4: occ = ring_occ_of<S, 4>(); break;
+      case 8: occ = ring_occ_of<S, 8>(); break;
+      case 12: occ = ring_occ_of<S, 12>(); break;
+      default: occ = ring_occ_of<S, 6>(); break;
+    }
+  }
+  return occ;
+}
+
+template <class S>
+int instance_kernel_occupancy() {
+  static int occ = -1;
+  if (occ < 0) {
+    cudaFuncSetAttribute(instance_hull_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)inst_smem_bytes<S>());
     int o = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, slab_hull_kernel<S>, kThreads, slab_smem_bytes<S>());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, instance_hull_kernel<S>, kThreads, inst_smem_bytes<S>());
     occ = o > 0 ? o : 1;
   }
   return occ;
@@ -523,13 +1355,24 @@ int slab_kernel_occupancy() {
 
 template <class S>
 void launch_slab_kernel(const SlabParams<S>& p, const CUtensorMap* tmap, int grid, cudaStream_t st) {
+  if (!p.hmode) {
+    instance_kernel_occupancy<S>();
+    instance_hull_kernel<S><<<grid, kThreads, inst_smem_bytes<S>(), st>>>(*tmap, p);
+    return;
+  }
   slab_kernel_occupancy<S>();
-  slab_hull_kernel<S><<<grid, kThreads, slab_smem_bytes<S>(), st>>>(*tmap, p);
+  switch (ring_depth()) {
+    case 4: ring_hull_kernel<S, 4><<<grid, 128, ring_smem<S, 4>(), st>>>(p); break;
+    case 8: ring_hull_kernel<S, 8><<<grid, 128, ring_smem<S, 8>(), st>>>(p); break;
+    case 12: ring_hull_kernel<S, 12><<<grid, 128, ring_smem<S, 12>(), st>>>(p); break;
+    default: ring_hull_kernel<S, 6><<<grid, 128, ring_smem<S, 6>(), st>>>(p); break;
+  }
 }
 
 size_t finalize_smem(int fcap_bytes, int slabs) {
-  return (size_t)slabs * (2 * sizeof(long long) + 2 * sizeof(double) + 3 * sizeof(int)) + 64 + 16 +
-         (size_t)fcap_bytes;
+  // tree nodes + scan scratch + 256 candidates + F (corners) + F flags
+  return (size_t)slabs * (sizeof(long long) + sizeof(int)) + 512 + 256 * (8 + 4 + 8 + 12) + 64 +
+         (size_t)fcap_bytes + (size_t)fcap_bytes / 2;
 }
 
 template <class S>
@@ -561,7 +1404,11 @@ template void launch_pad_fill<float>(void*, const void*, const int*, long long, 
 template void launch_pad_fill<double>(void*, const void*, const int*, long long, long long, cudaStream_t);
 template int slab_kernel_occupancy<float>();
 template int slab_kernel_occupancy<double>();
-template size_t slab_kernel_smem<float>();
-template size_t slab_kernel_smem<double>();
+template int instance_kernel_occupancy<float>();
+template int instance_kernel_occupancy<double>();
+template int slab_warps_per_cta<float>();
+template int slab_warps_per_cta<double>();
+template int slab_tile_rows<float>(bool);
+template int slab_tile_rows<double>(bool);
 
 }  // namespace hood_b200

@@ -12,7 +12,7 @@ constexpr int kThreads = 256;       // one 128-byte chunk row per thread
 constexpr int kStages = 3;          // TMA pipeline depth per CTA
 constexpr int kTileBytes = kThreads * 128;
 constexpr int kHCap = 1024;         // running slab hull kept in smem up to this many corners
-constexpr int kMaxSlabsPerInstance = 1024;
+constexpr int kMaxSlabsPerInstance = 2048;
 
 // First error of a build, encoded as key = index*2 + (x_not_increasing ? 1 : 0)
 // so one atomicMin keeps validate_points' order (hoodbuf.cpp:48-58: at the
@@ -26,6 +26,7 @@ struct SlabParams {
   const void* pts;          // n points, {x, y} interleaved, 16-byte aligned
   long long n;
   long long L;              // instance length (== n for a single instance)
+  int log2L;                // instance mode: L == 1 << log2L
   int hmode;                // 1: slabs with a running hull; 0: whole instances per tile (L < T)
   int seg_chunks;           // chunks per culling segment: 256 (hmode) or L/K
   long long tiles_per_inst; // hmode: ceil(L / T)
@@ -42,6 +43,10 @@ struct SlabParams {
   long long* seg_base;
   DevError* err;
   int check_range;          // also flag x outside (0,1) (validate_points)
+  int dbg;                  // 0 normal; 1 stream only (profiling); 2 no merger work
+  long long* trace;         // optional per-tile clock64 trace (profiling)
+  long long read_lim;       // points at or past this index may not be read yet (host-path chunks)
+  unsigned* pub;            // per unit: order-preserving key of its running max y (zeroed per build)
 };
 
 template <class S>
@@ -65,9 +70,13 @@ template <class S>
 void launch_pad_fill(void* padded, const void* corners, const int* counts, long long n, long long L,
                      cudaStream_t st);
 template <class S>
-int slab_kernel_occupancy();
+int slab_kernel_occupancy();    // slab-kernel CTAs per SM
 template <class S>
-size_t slab_kernel_smem();
+int instance_kernel_occupancy();  // instance-kernel CTAs per SM
+template <class S>
+int slab_warps_per_cta();      // units (warps) per slab-kernel CTA
+template <class S>
+int slab_tile_rows(bool hmode);  // chunk rows (= threads) per tile
 size_t finalize_smem(int fcap_bytes, int slabs);
 
 }  // namespace hood_b200

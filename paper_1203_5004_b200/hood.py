@@ -36,6 +36,7 @@ EXPORTS = [
     "hood_create", "hood_destroy", "hood_reserve", "hood_build_f32", "hood_build_f64",
     "hood_build_host_f32", "hood_build_host_f64", "hood_merge_segments_f32", "hood_merge_segments_f64",
     "hood_last_error", "hood_last_launch_count", "hood_status_string", "hood_abi_version",
+    "hood_set_profile_events",
 ]
 
 
@@ -82,6 +83,7 @@ def library():
                 getattr(L, nm).argtypes = [p, p, p, i64, i64, p, p, p]
             L.hood_last_error.argtypes = [p, ctypes.POINTER(_Err)]
             L.hood_last_launch_count.argtypes = [p]
+            L.hood_set_profile_events.argtypes = [p, p, p]
             L.hood_status_string.restype = ctypes.c_char_p
             L.hood_status_string.argtypes = [ctypes.c_int]
             for nm in EXPORTS:
@@ -136,6 +138,11 @@ class Context:
 
     def last_launch_count(self) -> int:
         return library().hood_last_launch_count(self.handle)
+
+    def set_profile_events(self, before=None, after=None):
+        """torch.cuda.Event pair recorded around the slab kernel of later builds."""
+        library().hood_set_profile_events(self.handle, before.cuda_event if before is not None else None,
+                                          after.cuda_event if after is not None else None)
 
     def reserve(self, n: int, block_len: int = 0, f64: bool = False):
         rc = library().hood_reserve(self.handle, n, block_len, int(f64))
