@@ -28,7 +28,7 @@ struct hood_ctx {
   int sms = 148;
   // device workspace
   int* seg_cnt = nullptr;
-  void* seg_ymax = nullptr;  // double-sized slots (fits float too)
+  void* seg_apt = nullptr;  // double2-sized slots (fits float2 too)
   long long* seg_base = nullptr;
   unsigned* pub = nullptr;
   long long seg_cap = 0;
@@ -124,12 +124,12 @@ int ensure_ws(hood_ctx* ctx, long long slabs) {
   }
   if (slabs > ctx->seg_cap) {
     cudaFree(ctx->seg_cnt);
-    cudaFree(ctx->seg_ymax);
+    cudaFree(ctx->seg_apt);
     cudaFree(ctx->seg_base);
     cudaFree(ctx->pub);
     const long long cap = std::max(slabs, 4096LL);
     if (cudaMalloc(&ctx->seg_cnt, cap * sizeof(int)) != cudaSuccess ||
-        cudaMalloc(&ctx->seg_ymax, cap * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&ctx->seg_apt, cap * 2 * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&ctx->seg_base, cap * sizeof(long long)) != cudaSuccess ||
         cudaMalloc(&ctx->pub, cap * sizeof(unsigned)) != cudaSuccess)
       return HOOD_ERR_CUDA;
@@ -178,7 +178,7 @@ SlabParams<S> slab_params(hood_ctx* ctx, const Plan& pl, const void* pts, void* 
   p.out = corners;
   p.out_counts = counts;
   p.seg_cnt = ctx->seg_cnt;
-  p.seg_ymax = reinterpret_cast<S*>(ctx->seg_ymax);
+  p.seg_apt = ctx->seg_apt;
   p.seg_base = ctx->seg_base;
   p.err = ctx->err;
   p.check_range = (flags & HOOD_FLAG_CHECK_RANGE) ? 1 : 0;
@@ -196,12 +196,13 @@ FinalizeParams<S> finalize_params(hood_ctx* ctx, const Plan& pl, void* corners, 
   f.out = corners;
   f.out_counts = counts;
   f.seg_cnt = ctx->seg_cnt;
-  f.seg_ymax = reinterpret_cast<const S*>(ctx->seg_ymax);
+  f.seg_apt = ctx->seg_apt;
   f.seg_base = ctx->seg_base;
   f.seg_stride = 0;
   f.slabs_per_inst = pl.spi;
   f.L = pl.L;
-  f.fcap = (int)((64 * 1024) / sizeof(V));
+  f.fcap = 2048;
+  f.trace = ctx->trace ? ctx->trace + 7 * 64 : nullptr;
   return f;
 }
 
@@ -214,6 +215,15 @@ void debug_check(const char* what, cudaStream_t st) {
   if (!on) return;
   const cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) std::fprintf(stderr, "[hood_b200] %s failed: %s\n", what, cudaGetErrorString(e));
+}
+
+// Event record that also works inside CUDA-graph capture (an external event
+// node, so the replay timestamps it).
+void record_event(cudaEvent_t ev, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal);
+  else cudaEventRecord(ev, st);
 }
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -234,10 +244,10 @@ int build_device(hood_ctx* ctx, const S* pts, long long n, long long block_len, 
   if (!pl.hmode && (rc = encode_map<S>(pts, n, pl.rows, &map, &full_rows))) return rc;
   if (cudaMemsetAsync(ctx->err, 0xff, sizeof(DevError), st) != cudaSuccess) return HOOD_ERR_CUDA;
   const SlabParams<S> p = slab_params<S>(ctx, pl, pts, corners, counts, full_rows, flags);
-  if (ctx->prof_before) cudaEventRecord(ctx->prof_before, st);
+  if (ctx->prof_before) record_event(ctx->prof_before, st);
   launch_slab_kernel<S>(p, &map, pl.grid, st);
   debug_check("slab kernel", st);
-  if (ctx->prof_after) cudaEventRecord(ctx->prof_after, st);
+  if (ctx->prof_after) record_event(ctx->prof_after, st);
   int launches = 1;
   if (pl.hmode && pl.spi > 1) {
     launch_finalize<S>(finalize_params<S>(ctx, pl, corners, counts), (int)pl.instances, st);
@@ -389,12 +399,12 @@ int merge_segments(hood_ctx* ctx, const S* seg_pts, const int* counts, long long
   f.out = corners;
   f.out_counts = count;
   f.seg_cnt = ctx->seg_cnt;
-  f.seg_ymax = nullptr;
+  f.seg_apt = nullptr;
   f.seg_base = nullptr;
   f.seg_stride = stride;
   f.slabs_per_inst = (int)G;
   f.L = G * stride;
-  f.fcap = (int)((64 * 1024) / sizeof(V));
+  f.fcap = 2048;
   launch_finalize<S>(f, 1, st);
   ctx->last_stream = st;
   ctx->have_last = true;
@@ -427,7 +437,7 @@ int hood_destroy(hood_ctx* c) {
   if (!c) return HOOD_OK;
   cudaSetDevice(c->device);
   cudaFree(c->seg_cnt);
-  cudaFree(c->seg_ymax);
+  cudaFree(c->seg_apt);
   cudaFree(c->seg_base);
   cudaFree(c->pub);
   cudaFree(c->err);

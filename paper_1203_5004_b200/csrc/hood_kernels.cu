@@ -122,6 +122,23 @@ __device__ __forceinline__ void st_relaxed(unsigned* p, unsigned v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+template <class V> __device__ __forceinline__ V make_vec(decltype(V::x) x, decltype(V::x) y) { return V{x, y}; }
+
+// Point of maximal y over the warp (exact; ties keep either).
+template <class V>
+__device__ __forceinline__ V warp_argmax_y(V p) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const auto ox = __shfl_xor_sync(0xffffffffu, p.x, o);
+    const auto oy = __shfl_xor_sync(0xffffffffu, p.y, o);
+    if (oy > p.y) {
+      p.x = ox;
+      p.y = oy;
+    }
+  }
+  return p;
+}
+
 // Warp maximum through one REDUX on an order-preserving 32-bit key.  Exact
 // for float; a double is rounded toward -inf first, so the result never
 // exceeds the true maximum (still a valid anchor height).
@@ -834,16 +851,38 @@ __global__ void __launch_bounds__(128) ring_hull_kernel(const SlabParams<S> p) {
     }
     cp_async_wait<0>();
     __syncwarp();
+    (void)umax;
 
     if (hs.in_smem)
       for (long long e = lane; e < hs.n; e += 32) gout[ubase + e] = Hs[e];
+    if (spi > 1) {
+      // anchor point for finalize: the unit's highest hood corner (a real
+      // input point; y along a hood is unimodal, so a spilled hood is searched)
+      V apt = make_vec<V>(NEG, NEG);
+      if (hs.n > 0) {
+        if (hs.in_smem) {
+          for (long long e = lane; e < hs.n; e += 32)
+            if (Hs[e].y > apt.y) apt = Hs[e];
+          apt = warp_argmax_y(apt);
+        } else if (lane == 0) {
+          const V* h = gout + ubase;
+          long long a = 0, b = hs.n - 1;
+          while (a < b) {
+            const long long mid = (a + b) >> 1;
+            if (h[mid + 1].y > h[mid].y) a = mid + 1;
+            else b = mid;
+          }
+          apt = h[a];
+        }
+      }
+      if (lane == 0) reinterpret_cast<V*>(p.seg_apt)[u] = apt;
+    }
     if (lane == 0) {
       if (spi == 1) {
         p.out_counts[inst] = (int)hs.n;
       } else {
         p.seg_cnt[u] = (int)hs.n;
         p.seg_base[u] = ubase;
-        p.seg_ymax[u] = umax;
       }
     }
     __syncwarp();
@@ -1021,237 +1060,276 @@ __device__ __forceinline__ T block_excl_scan(T v, T ident, Op op, T* sh, bool re
   return op(carry, exc);
 }
 
+// Block-wide exclusive "highest point" scan (blockDim = FT): for every thread,
+// the point of maximal y among the threads before (or after) it.
+template <class V, int NWP>
+__device__ __forceinline__ V block_excl_argmax(V v, V ident, V* sh, bool reverse) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  V inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    V a;
+    a.x = reverse ? __shfl_down_sync(0xffffffffu, inc.x, o) : __shfl_up_sync(0xffffffffu, inc.x, o);
+    a.y = reverse ? __shfl_down_sync(0xffffffffu, inc.y, o) : __shfl_up_sync(0xffffffffu, inc.y, o);
+    if ((reverse ? (lane + o < 32) : (lane >= o)) && a.y > inc.y) inc = a;
+  }
+  V exc;
+  exc.x = reverse ? __shfl_down_sync(0xffffffffu, inc.x, 1) : __shfl_up_sync(0xffffffffu, inc.x, 1);
+  exc.y = reverse ? __shfl_down_sync(0xffffffffu, inc.y, 1) : __shfl_up_sync(0xffffffffu, inc.y, 1);
+  if (reverse ? lane == 31 : lane == 0) exc = ident;
+  if (reverse ? lane == 0 : lane == 31) sh[warp] = inc;
+  __syncthreads();
+  V carry = ident;
+  for (int w = 0; w < NWP; ++w)
+    if ((reverse ? (w > warp) : (w < warp)) && sh[w].y > carry.y) carry = sh[w];
+  __syncthreads();
+  return exc.y > carry.y ? exc : carry;
+}
+
+// Block-wide exclusive prefix sum (blockDim = 32 * NWP).
+template <int NWP>
+__device__ __forceinline__ int block_excl_sum(int v, int* sh, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int a = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += a;
+  }
+  if (lane == 31) sh[warp] = inc;
+  __syncthreads();
+  int carry = 0, tot = 0;
+  for (int w = 0; w < NWP; ++w) {
+    if (w < warp) carry += sh[w];
+    tot += sh[w];
+  }
+  __syncthreads();
+  *total = tot;
+  return carry + inc - v;
+}
+
+constexpr int kFinThreads = 256;
+constexpr int kFinCand = 128;      // candidate slabs handled in smem
+constexpr int kFinCandCap = 32;    // corners staged per candidate
+
+// Final merge of the slab hoods of one instance (one CTA per instance).
+//   1. Every slab carries an anchor point, its highest hood corner.  For slab
+//      s, A = the highest anchor left of it and C = the highest right of it;
+//      a corner of s on or below the chord A-C cannot be a corner of the
+//      final hood (it is not strictly above a chord of two input points that
+//      straddle it).  Slabs whose highest corner is below both A and C go
+//      without a single corner read.
+//   2. One warp per remaining slab reads its corners coalesced and stages the
+//      run strictly above A-C (one contiguous run: a concave chain meets a
+//      line once) in smem; the runs are then compacted in x order.
+//   3. The survivors are pruned in parallel rounds: a point not strictly
+//      above the chord of its current neighbours is not a hull corner and is
+//      dropped (geom.hpp:22-28 predicate, canonical order); when a round drops
+//      nothing the chain is strictly concave, i.e. the strict upper hull --
+//      exactly what oracle.cpp:7-20 returns.
+// Huge survivor sets (the arc) merge the slab hoods in place in HBM instead.
 template <class S>
-__global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams<S> p) {
+__global__ void __launch_bounds__(kFinThreads, 1) finalize_kernel(const FinalizeParams<S> p) {
   using V = typename PointT<S>::V;
+  constexpr int NWP = kFinThreads / 32;
+  constexpr int R = kMaxSlabsPerInstance / kFinThreads;  // segments per thread (at most)
+  constexpr int MAXC = kFinCand, CAP = kFinCandCap;
   extern __shared__ unsigned char smem_raw[];
-  constexpr int R = kMaxSlabsPerInstance / 256;  // segments per thread (at most)
-  constexpr int MAXC = 256;                      // culling candidates handled in smem
   const int M = p.slabs_per_inst;
   const long long s0 = (long long)blockIdx.x * M;
   const long long ibase = (long long)blockIdx.x * p.L;
   V* gout = reinterpret_cast<V*>(p.out);
   const S NEG = neg_inf<S>();
+  const V NOPT = V{NEG, NEG};
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   long long* nsd = reinterpret_cast<long long*>(smem_raw);  // [M] tree path
   int* ncd = reinterpret_cast<int*>(nsd + M);               // [M]
-  S* shS = reinterpret_cast<S*>((reinterpret_cast<uintptr_t>(ncd + M) + 15) & ~(uintptr_t)15);  // [8]
-  int* shI = reinterpret_cast<int*>(shS + 8);               // [16]
-  long long* cb = reinterpret_cast<long long*>((reinterpret_cast<uintptr_t>(shI + 16) + 7) & ~(uintptr_t)7);  // [MAXC] base
-  int* cc = reinterpret_cast<int*>(cb + MAXC);              // [MAXC] count
-  S* ct = reinterpret_cast<S*>((reinterpret_cast<uintptr_t>(cc + MAXC) + 15) & ~(uintptr_t)15);  // [MAXC] tau
-  int* clo = reinterpret_cast<int*>(ct + MAXC);             // [MAXC] alive start
-  int* cn = clo + MAXC;                                     // [MAXC] alive count
-  int* coff = cn + MAXC;                                    // [MAXC] offset in F
-  V* F = reinterpret_cast<V*>((reinterpret_cast<uintptr_t>(coff + MAXC) + 15) & ~(uintptr_t)15);
+  V* shV = reinterpret_cast<V*>((reinterpret_cast<uintptr_t>(ncd + M) + 15) & ~(uintptr_t)15);  // [NWP]
+  int* shI = reinterpret_cast<int*>(shV + NWP);             // [NWP + 8]
+  long long* cb = reinterpret_cast<long long*>((reinterpret_cast<uintptr_t>(shI + NWP + 8) + 7) & ~(uintptr_t)7);  // [MAXC]
+  int* cc = reinterpret_cast<int*>(cb + MAXC);              // [MAXC] corner count
+  int* cn = cc + MAXC;                                      // [MAXC] alive count
+  V* cA = reinterpret_cast<V*>((reinterpret_cast<uintptr_t>(cn + MAXC) + 15) & ~(uintptr_t)15);  // [MAXC]
+  V* cC = cA + MAXC;                                        // [MAXC]
+  V* stg = cC + MAXC;                                       // [MAXC][CAP] staged alive runs
+  V* F = stg + MAXC * CAP;                                  // [2][fcap] ping-pong survivors
 
-  // 1. thread t owns the consecutive segments [t*per, t*per + per)
-  const int per = (M + 255) / 256;
+  if (p.trace && tid == 0) p.trace[0] = clock64();
+  const int per = (M + kFinThreads - 1) / kFinThreads;
   long long sb[R];
   int sc[R];
-  S sy[R];
+  V ap[R];
 #pragma unroll
   for (int j = 0; j < R; ++j) {
     const int s = tid * per + j;
     sb[j] = 0;
     sc[j] = 0;
-    sy[j] = NEG;
+    ap[j] = NOPT;
     if (j < per && s < M) {
       sb[j] = p.seg_base ? p.seg_base[s0 + s] : ibase + (long long)s * p.seg_stride;
       sc[j] = p.seg_cnt[s0 + s];
-      if (p.seg_ymax) {
-        sy[j] = p.seg_ymax[s0 + s];
+      if (p.seg_apt) {
+        ap[j] = reinterpret_cast<const V*>(p.seg_apt)[s0 + s];
       } else {
-        for (int e = 0; e < sc[j]; ++e) sy[j] = fmax(sy[j], gout[sb[j] + e].y);
+        for (int e = 0; e < sc[j]; ++e)
+          if (gout[sb[j] + e].y > ap[j].y) ap[j] = gout[sb[j] + e];
       }
     }
   }
-  S tmax = NEG;
+  V tbest = NOPT;
 #pragma unroll
-  for (int j = 0; j < R; ++j) tmax = fmax(tmax, sy[j]);
-  auto mx = [](S a, S b) { return fmax(a, b); };
-  const S pre_t = block_excl_scan<S>(tmax, NEG, mx, shS, false);
-  const S suf_t = block_excl_scan<S>(tmax, NEG, mx, shS, true);
+  for (int j = 0; j < R; ++j)
+    if (ap[j].y > tbest.y) tbest = ap[j];
+  if (p.trace && tid == 0) p.trace[1] = clock64();
+  const V pre_t = block_excl_argmax<V, NWP>(tbest, NOPT, shV, false);
+  const V suf_t = block_excl_argmax<V, NWP>(tbest, NOPT, shV, true);
 
-  // 2. anchor height of every segment: its corners below tau lie under the
-  //    chord between the maxima of a segment on each side; segments whose own
-  //    maximum is below tau vanish without a single corner read.  Survivors
-  //    ("candidates") are compacted in x order.
+  V aA[R], aC[R];
   bool cand[R];
-  S tauj[R];
   int ncand = 0;
   {
-    S pre = pre_t;
+    V pre = pre_t;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
-      S suf = suf_t;
+      V suf = suf_t;
 #pragma unroll
-      for (int jj = j + 1; jj < R; ++jj) suf = fmax(suf, sy[jj]);
-      tauj[j] = fmin(pre, suf);
-      pre = fmax(pre, sy[j]);
-      cand[j] = sc[j] > 0 && !(sy[j] < tauj[j]);
+      for (int jj = j + 1; jj < R; ++jj)
+        if (ap[jj].y > suf.y) suf = ap[jj];
+      aA[j] = pre;
+      aC[j] = suf;
+      if (ap[j].y > pre.y) pre = ap[j];
+      cand[j] = sc[j] > 0 && !(ap[j].y < fmin(aA[j].y, aC[j].y));
       ncand += cand[j];
     }
   }
-  auto add = [](int a, int b) { return a + b; };
-  int coff0 = block_excl_scan<int>(ncand, 0, add, shI, false);
-  if (tid == 255) shI[8] = coff0 + ncand;
-  __syncthreads();
-  const int C = shI[8];
-  __syncthreads();
-  const bool small = C <= MAXC;
-  if (small) {
+  int C;
+  int cpos = block_excl_sum<NWP>(ncand, shI, &C);
+  if (p.trace && tid == 0) p.trace[2] = clock64();
+
+  if (C <= MAXC) {
 #pragma unroll
     for (int j = 0; j < R; ++j)
       if (cand[j]) {
-        cb[coff0] = sb[j];
-        cc[coff0] = sc[j];
-        ct[coff0] = tauj[j];
-        ++coff0;
+        cb[cpos] = sb[j];
+        cc[cpos] = sc[j];
+        cA[cpos] = aA[j];
+        cC[cpos] = aC[j];
+        ++cpos;
       }
-  }
-  __syncthreads();
-
-  if (small) {
-    // 3. one warp per candidate: coalesced corner loads, alive run = the
-    //    corners with y >= tau (contiguous: y is unimodal along a hood)
-    for (int c = warp; c < C; c += 8) {
+    __syncthreads();
+    // one warp per candidate: stage its corners strictly above the chord A-C
+    for (int c = warp; c < C; c += NWP) {
       const long long b = cb[c];
       const int cnt = cc[c];
-      const S tau = ct[c];
-      int first = 0x7fffffff, last = -1;
-      for (int e = lane; e < cnt; e += 32)
-        if (!(gout[b + e].y < tau)) {
-          first = min(first, e);
-          last = max(last, e);
+      const V A = cA[c], Cp = cC[c];
+      const bool both = A.y > NEG && Cp.y > NEG;  // without both anchors nothing is culled
+      int n_alive = 0;
+      for (int e0 = 0; e0 < cnt; e0 += 32) {
+        const int e = e0 + lane;
+        V v = NOPT;
+        bool keep = false;
+        if (e < cnt) {
+          v = gout[b + e];
+          keep = !both || above(A, v, Cp);
         }
-      first = __reduce_min_sync(0xffffffffu, first);
-      last = __reduce_max_sync(0xffffffffu, last);
-      if (lane == 0) {
-        clo[c] = last >= 0 ? first : 0;
-        cn[c] = last >= 0 ? last - first + 1 : 0;
+        const unsigned mk = __ballot_sync(0xffffffffu, keep);
+        const int pos = n_alive + __popc(mk & ((1u << lane) - 1u));
+        if (keep && pos < CAP) stg[c * CAP + pos] = v;
+        n_alive += __popc(mk);
       }
+      if (lane == 0) cn[c] = n_alive;
     }
     __syncthreads();
-    // 4. offsets of the alive runs (x order) and their total
-    const int mine = tid < C ? cn[tid] : 0;
-    int off = 0;
-    {
-      int acc = 0;
-      for (int base = 0; base < C; base += 256) {
-        const int v = (base + tid < C) ? cn[base + tid] : 0;
-        const int o = block_excl_scan<int>(v, 0, add, shI, false);
-        if (base + tid < C) coff[base + tid] = acc + o;
-        if (tid == 255) shI[9] = o + v;
-        __syncthreads();
-        acc += shI[9];
-        __syncthreads();
+    if (p.trace && tid == 0) p.trace[3] = clock64();
+    int ovf = 0, A = 0;
+    for (int c = tid; c < C; c += kFinThreads) ovf |= cn[c] > CAP;
+    ovf = __syncthreads_or(ovf);
+    const int v0 = tid < C ? min(cn[tid], CAP) : 0;
+    const int o0 = block_excl_sum<NWP>(v0, shI, &A);
+    if (!ovf && A <= p.fcap) {
+      V* Fa = F;
+        // compact the staged runs in x order; each run is a strict hood
+      long long* rns = nsd;  // reuse the tree-node arrays: run start / size
+      int* rnc = ncd;
+      if (tid < C) {
+        for (int e = 0; e < cn[tid]; ++e) Fa[o0 + e] = stg[tid * CAP + e];
+        rns[tid] = o0;
+        rnc[tid] = cn[tid];
       }
-      off = acc;  // total alive corners (uniform)
-      (void)mine;
-    }
-    const int A = off;
-    if (A <= p.fcap) {
-      for (int c = warp; c < C; c += 8)
-        for (int e = lane; e < cn[c]; e += 32) F[coff[c] + e] = gout[cb[c] + clo[c] + e];
       __syncthreads();
-      // 5. exact strict hull of the A x-sorted survivors.  Point i is a corner
-      //    iff it lies strictly above the chord (a*, b*) joining the point of
-      //    minimal slope to it from the left and of maximal slope from it to
-      //    the right (all canonical predicates); the end points always are.
-      int* flag = reinterpret_cast<int*>(F + A);
-      if (A <= 1024) {
-        for (int i = tid; i < A; i += 256) {
-          int keep = 1;
-          if (i > 0 && i + 1 < A) {
-            const V q = F[i];
-            int as = 0;
-            for (int a = 1; a < i; ++a)
-              if (above(F[as], F[a], q)) as = a;  // slope(a, i) < slope(as, i)
-            int bs = i + 1;
-            for (int b = i + 2; b < A; ++b)
-              if (orient_sign(q, F[bs], F[b]) < 0) bs = b;  // slope(i, b) > slope(i, bs)
-            keep = above(F[as], q, F[bs]) ? 1 : 0;
+      if (p.trace && tid == 0) p.trace[4] = clock64();
+      // one monotone chain (oracle.cpp:7-20) over the few survivors, in
+      // place (the stack never passes the point being read)
+      if (tid == 0) {
+        int h = 0;
+        V h1 = V{}, h2 = V{};
+        for (int i = 0; i < A; ++i) {
+          const V q = Fa[i];
+          while (h >= 2 && !above(h2, h1, q)) {
+            --h;
+            h1 = h2;
+            if (h >= 2) h2 = Fa[h - 2];
           }
-          flag[i] = keep;
+          Fa[h] = q;
+          ++h;
+          h2 = h1;
+          h1 = q;
         }
-        __syncthreads();
-        // compact the corners in order
-        int w = 0;
-        {
-          int acc = 0;
-          for (int base = 0; base < A; base += 256) {
-            const int v = (base + tid < A) ? flag[base + tid] : 0;
-            const int o = block_excl_scan<int>(v, 0, add, shI, false);
-            if (base + tid < A && v) gout[ibase + acc + o] = F[base + tid];
-            if (tid == 255) shI[10] = o + v;
-            __syncthreads();
-            acc += shI[10];
-            __syncthreads();
-          }
-          w = acc;
-        }
-        if (tid == 0) p.out_counts[blockIdx.x] = w;
-      } else {
-        // larger: one monotone chain (oracle.cpp:7-20) in place
-        if (tid == 0) {
-          int h = 0;
-          V h1 = V{}, h2 = V{};
-          for (int i = 0; i < A; ++i) {
-            const V q = F[i];
-            while (h >= 2 && !above(h2, h1, q)) {
-              --h;
-              h1 = h2;
-              if (h >= 2) h2 = F[h - 2];
-            }
-            F[h] = q;
-            ++h;
-            h2 = h1;
-            h1 = q;
-          }
-          shI[11] = h;
-        }
-        __syncthreads();
-        const int hc = shI[11];
-        for (int e = tid; e < hc; e += blockDim.x) gout[ibase + e] = F[e];
-        if (tid == 0) p.out_counts[blockIdx.x] = hc;
+        rns[0] = 0;
+        rnc[0] = h;
+      }
+      __syncthreads();
+      if (p.trace && tid == 0) p.trace[5] = clock64();
+      const long long rs = rns[0];
+      const int n = rnc[0];
+      for (int e = tid; e < n; e += kFinThreads) gout[ibase + e] = Fa[rs + e];
+      if (tid == 0) p.out_counts[blockIdx.x] = n;
+      if (p.trace && tid == 0) {
+        p.trace[6] = clock64();
+        p.trace[7] = clock64();
+        p.trace[8] = A;
+        p.trace[9] = C;
       }
       return;
     }
   }
 
   // huge hoods (the arc, many candidates): merge tree over the slab hoods in
-  // place in HBM, each slab's alive run found with the unimodal y searches
+  // place in HBM; every slab keeps its run strictly above its chord A-C
+  // (found with binary searches: the run is contiguous and the height above
+  // the chord is unimodal along the hood)
 #pragma unroll
   for (int j = 0; j < R; ++j) {
     const int s = tid * per + j;
     if (j < per && s < M) {
-      int l = 0, r = 0;
-      const int c = sc[j];
-      const S tau = tauj[j];
+      int l = 0, r = sc[j];
+      const V A = aA[j], Cp = aC[j];
       const V* h = gout + sb[j];
-      if (c > 0 && !(sy[j] < tau)) {
-        r = c;
-        if (!(h[0].y >= tau && h[c - 1].y >= tau)) {
-          int a = 0, bq = c - 1;
-          while (a < bq) {
-            const int mid = (a + bq) >> 1;
-            if (h[mid + 1].y > h[mid].y) a = mid + 1;
-            else bq = mid;
-          }
-          const int pk = a;
+      const int c = sc[j];
+      if (c > 0 && A.y > NEG && Cp.y > NEG && !(above(A, h[0], Cp) && above(A, h[c - 1], Cp))) {
+        int a = 0, bq = c - 1;
+        while (a < bq) {
+          const int mid = (a + bq) >> 1;
+          const V d = V{h[mid].x + (Cp.x - A.x), h[mid].y + (Cp.y - A.y)};
+          if (orient_sign(h[mid], h[mid + 1], d) > 0) a = mid + 1;
+          else bq = mid;
+        }
+        const int pk = a;
+        if (!above(A, h[pk], Cp)) {
+          l = r = 0;
+        } else {
           int x0 = 0, x1 = pk;
           while (x0 < x1) {
             const int mid = (x0 + x1) >> 1;
-            if (h[mid].y >= tau) x1 = mid;
+            if (above(A, h[mid], Cp)) x1 = mid;
             else x0 = mid + 1;
           }
           l = x0;
           int y0 = pk, y1 = c - 1;
           while (y0 < y1) {
             const int mid = (y0 + y1 + 1) >> 1;
-            if (h[mid].y >= tau) y0 = mid;
+            if (above(A, h[mid], Cp)) y0 = mid;
             else y1 = mid - 1;
           }
           r = y0 + 1;
@@ -1370,9 +1448,10 @@ void launch_slab_kernel(const SlabParams<S>& p, const CUtensorMap* tmap, int gri
 }
 
 size_t finalize_smem(int fcap_bytes, int slabs) {
-  // tree nodes + scan scratch + 256 candidates + F (corners) + F flags
-  return (size_t)slabs * (sizeof(long long) + sizeof(int)) + 512 + 256 * (8 + 4 + 8 + 12) + 64 +
-         (size_t)fcap_bytes + (size_t)fcap_bytes / 2;
+  // tree nodes + scan scratch + candidates (base, 2 ints, 2 anchor points,
+  // staged runs) + two survivor buffers; sized for double2 points
+  return (size_t)slabs * (sizeof(long long) + sizeof(int)) + 1024 +
+         (size_t)kFinCand * (8 + 8 + 32 + (size_t)kFinCandCap * 16) + 2 * (size_t)fcap_bytes + 64;
 }
 
 template <class S>
@@ -1381,10 +1460,10 @@ void launch_finalize(const FinalizeParams<S>& p, int instances, cudaStream_t st)
   const size_t bytes = finalize_smem(p.fcap * (int)sizeof(V), p.slabs_per_inst);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(finalize_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(finalize_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  finalize_kernel<S><<<instances, 256, bytes, st>>>(p);
+  finalize_kernel<S><<<instances, kFinThreads, bytes, st>>>(p);
 }
 
 template <class S>

@@ -39,7 +39,7 @@ struct SlabParams {
   void* out;                // corner slots (n), instance i at [i*L, i*L+count)
   int* out_counts;          // per instance
   int* seg_cnt;             // per slab (hmode)
-  S* seg_ymax;
+  void* seg_apt;            // per slab: its highest hood corner (anchor point for finalize)
   long long* seg_base;
   DevError* err;
   int check_range;          // also flag x outside (0,1) (validate_points)
@@ -54,12 +54,13 @@ struct FinalizeParams {
   void* out;
   int* out_counts;
   const int* seg_cnt;
-  const S* seg_ymax;        // nullptr: compute from the segment corners
+  const void* seg_apt;      // per segment anchor point (its highest corner); nullptr: scan the corners
   const long long* seg_base; // nullptr: segment s starts at s * seg_stride
   long long seg_stride;
   int slabs_per_inst;
   long long L;
   int fcap;                 // smem corner capacity of the fast path
+  long long* trace;         // optional phase clock64 stamps (profiling)
 };
 
 template <class S>

@@ -16,7 +16,7 @@ pts = W.grid_uniform_torch(n, seed=2) if cfg == 2 else W.gauss_torch(n, seed=4)
 L = H.library()
 L.hood_internal_set_debug.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
 ctx = H.Context.get(0)
-trace = torch.zeros(8 * 64, dtype=torch.int64, device="cuda")
+trace = torch.zeros(16 * 64, dtype=torch.int64, device="cuda")
 flush = torch.empty(64 << 20, dtype=torch.int32, device="cuda")
 corners = torch.empty_like(pts); counts = torch.empty(1, dtype=torch.int32, device="cuda")
 for mode in [0, 1, 2, 0]:
@@ -32,7 +32,9 @@ for mode in [0, 1, 2, 0]:
         ts.append(a.elapsed_time(b))
     ctx.set_profile_events(None, None)
     print(f"mode {mode}: slab kernel {sorted(ts)[len(ts)//2]*1e3:.1f} us  ({n * pts.element_size() * 2 / (sorted(ts)[len(ts)//2]*1e-3) / 1e9:.0f} GB/s)")
-    tr = trace.view(8, 64).cpu()
+    tr = trace.view(16, 64).cpu()
+    f = trace[7 * 64: 7 * 64 + 10].cpu().tolist()
+    if mode == 0: print('finalize phases', [f[i + 1] - f[i] for i in range(6)], 'A', f[8], 'C', f[9])
     t0 = int(tr[0, 0])
     rows = ["iter", "nextrdy", "checked", "folded", "produced", "-", "survivors"]
     if mode == 0:
