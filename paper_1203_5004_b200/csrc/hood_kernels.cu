@@ -615,24 +615,57 @@ struct RingLayout {
   static constexpr size_t BYTES = up(MNC + 32 * 4, 128);
 };
 
+// Warp inclusive max-scans (toward higher lanes / toward lower lanes).
+template <class S>
+__device__ __forceinline__ S scan_up_max(S v, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const S o = __shfl_up_sync(0xffffffffu, v, d);
+    if (lane >= d) v = fmax(v, o);
+  }
+  return v;
+}
+template <class S>
+__device__ __forceinline__ S scan_down_max(S v, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const S o = __shfl_down_sync(0xffffffffu, v, d);
+    if (lane + d < 32) v = fmax(v, o);
+  }
+  return v;
+}
+
+// Position of one warp in its sequence of units: the unit with serial r
+// (u = unit_lo + gw + r * nwarps) and the block range [b, e) still ahead of
+// the cursor (global block indices).  Past the last unit b >= e.
+struct UnitCur {
+  int r;
+  long long b, e;
+};
+
 // The hot kernel.  Every warp is an independent pipeline over its own
-// contiguous x-range of the input (a "unit").  Its lanes stream the unit's 2 KB
-// blocks (256 float2 / 128 double2 points) with coalesced 16-byte cp.async into
-// a per-warp ring of R = D + 2 smem slots, D blocks ahead of the block being
-// processed.  A block's maximum y is taken when it lands; the block itself is
+// sequence of units (contiguous x-ranges of the input; a whole instance in
+// batched builds).  Its lanes stream the blocks (2 KB: 256 float2 / 128 double2
+// points) of that sequence with coalesced 16-byte cp.async into a per-warp
+// ring of R = D + 2 smem slots, D blocks ahead of the block being processed --
+// across unit boundaries, so short units (batched instances) never drain the
+// pipeline.  A block's maximum y is taken when it lands; the block itself is
 // processed D iterations later with
 //   left  = max y of the unit's earlier blocks (or of the EXT points before
 //           the unit),
-//   right = max y of the next D blocks (or of the EXT points after the unit),
+//   right = max y of the unit's next (up to D) blocks and of the EXT points
+//           after the unit,
 // both sets strictly left / right of every point of the block: a point below
 // min(left, right) lies strictly below the chord of two input points that
 // straddle it, cannot be a corner of the final hood (oracle.cpp:7-20 pops it)
-// and is dropped with one compare.  The rare survivors are compacted in x
-// order with ballots and folded into the warp's running hood (monotone-chain
-// pushes, or a warp merge tree + bridge -- kernel.hpp:31-67 -- when many).
-// x strictly increasing is checked on the way (validate_points,
-// hoodbuf.cpp:48-58).  Lanes only ever read the smem bytes they copied
-// themselves, so no barrier of any kind is needed.
+// and is dropped with one compare.  A block at an instance edge (no point on
+// one side) gets exact per-point anchors instead: warp max-scans over the block
+// in x order.  The rare survivors are compacted in x order with ballots and
+// folded into the unit's running hood (monotone-chain pushes, or a warp merge
+// tree + bridge -- kernel.hpp:31-67 -- when many).  x strictly increasing is
+// checked on the way (validate_points, hoodbuf.cpp:48-58).  Lanes only ever
+// read the smem bytes they copied themselves, so no barrier of any kind is
+// needed.
 template <class S, int D>
 __global__ void __launch_bounds__(128) ring_hull_kernel(const SlabParams<S> p) {
   using V = typename PointT<S>::V;
@@ -660,233 +693,325 @@ __global__ void __launch_bounds__(128) ring_hull_kernel(const SlabParams<S> p) {
 
   const int spi = p.slabs_per_inst;
   const long long bpi = p.tiles_per_inst;  // blocks per instance
+  const long long n = p.n;
+  const long long n_bytes = n * (long long)sizeof(V);
   const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
 
-  for (long long u = p.unit_lo + gw; u < p.unit_hi; u += nwarps) {
-    const int uu = (int)u, inst = uu / spi, jslab = uu - inst * spi;
-    const long long b0 = (long long)inst * bpi + ((long long)jslab * bpi) / spi;  // global block indices
-    const long long b1 = (long long)inst * bpi + ((long long)(jslab + 1) * bpi) / spi;
-    const int nblk = (int)(b1 - b0);
-    const long long ibase = (long long)inst * p.L;
-    const long long lim = min(p.n, ibase + p.L);
-    const long long ubase = b0 * BP;
-    const long long uend = min(b1 * BP, lim);
-    const int nfull = (int)min((long long)nblk, (lim - ubase) / BP);  // blocks [0, nfull) are full
-    const long long lim_bytes = lim * (long long)sizeof(V);
-
-    // copy block k of the unit into ring slot s (lane column); full blocks
-    // take four plain 16-byte copies, the input's last block is clamped
-    auto issue = [&](int k, int s) {
-      const long long off = (b0 + k) * (long long)BB;
-      unsigned char* dst = ring + s * BB;
-      if (k < nfull) {
-#pragma unroll
-        for (int j = 0; j < U; ++j) cp_async16(dst + j * 512, gbytes + off + j * 512, 16);
+  auto unit_of = [&](int r) -> long long { return p.unit_lo + gw + (long long)r * nwarps; };
+  auto seek = [&](UnitCur& c) {  // c.r set: load the block range of its unit
+    const long long u = unit_of(c.r);
+    if (u < p.unit_hi) {
+      if (spi == 1) {
+        c.b = u * bpi;
+        c.e = c.b + bpi;
       } else {
-#pragma unroll
-        for (int j = 0; j < U; ++j) {
-          const long long rem = lim_bytes - (off + lane * 16 + j * 512);
-          const int nb = rem >= 16 ? 16 : (rem > 0 ? (int)rem : 0);
-          cp_async16(dst + j * 512, nb ? gbytes + off + j * 512 : gbytes, nb);
-        }
+        const int uu = (int)u, inst = uu / spi, js = uu - inst * spi;
+        c.b = (long long)inst * bpi + ((long long)js * bpi) / spi;
+        c.e = (long long)inst * bpi + ((long long)(js + 1) * bpi) / spi;
       }
-    };
-    // max y of block k (slot s) over the warp; the partial block masks points
-    auto block_max = [&](int k, int s) -> S {
-      const unsigned char* src = ring + s * BB;
-      S m = NEG;
-      if (k < nfull) {
+    } else {
+      c.b = c.e = 0;
+    }
+  };
+  auto advance = [&](UnitCur& c) {
+    if (c.b < c.e && ++c.b == c.e) {
+      ++c.r;
+      seek(c);
+    }
+  };
+  // copy global block b into ring slot s (lane column); the input's last
+  // block is clamped (cp.async zero-fills the rest)
+  auto issue = [&](long long b, int s) {
+    const long long off = b * (long long)BB;
+    unsigned char* dst = ring + s * BB;
+    if ((b + 1) * BP <= n) {
 #pragma unroll
-        for (int j = 0; j < U; ++j) {
-          const L c = *reinterpret_cast<const L*>(src + j * 512);
+      for (int j = 0; j < U; ++j) cp_async16(dst + j * 512, gbytes + off + j * 512, 16);
+    } else {
 #pragma unroll
-          for (int e = 0; e < PPL; ++e) m = fmax(m, pt_of(c, e).y);
-        }
-      } else {
-        const long long q0 = ubase + (long long)k * BP + lane * PPL;
-#pragma unroll
-        for (int j = 0; j < U; ++j) {
-          const L c = *reinterpret_cast<const L*>(src + j * 512);
-#pragma unroll
-          for (int e = 0; e < PPL; ++e)
-            if (q0 + j * 32 * PPL + e < lim) m = fmax(m, pt_of(c, e).y);
-        }
+      for (int j = 0; j < U; ++j) {
+        const long long rem = n_bytes - (off + lane * 16 + j * 512);
+        const int nb = rem >= 16 ? 16 : (rem > 0 ? (int)rem : 0);
+        cp_async16(dst + j * 512, nb ? gbytes + off + j * 512 : gbytes, nb);
       }
-      return warp_max_fast(m);
-    };
-
-    // edge anchors: max y of up to EXT points on each side of the unit
-    S ext_l = NEG, ext_r = NEG;
-    {
-      const long long l0 = max(ibase, ubase - EXT);
-      for (long long i = l0 + lane; i < ubase; i += 32) ext_l = fmax(ext_l, gpts[i].y);
-      const long long r1 = min(min(lim, p.read_lim), uend + EXT);
-      for (long long i = uend + lane; i < r1; i += 32) ext_r = fmax(ext_r, gpts[i].y);
-      ext_l = warp_max(ext_l);
-      ext_r = warp_max(ext_r);
     }
-
-    // prologue: blocks 0 .. D in flight (one commit group each); maxima of
-    // blocks 1 .. D-1 into the window (block D's comes with iteration 0)
+  };
+  // max y of global block b (slot s) over the warp; missing points masked
+  auto block_max = [&](long long b, int s) -> S {
+    const unsigned char* src = ring + s * BB;
+    S m = NEG;
+    if ((b + 1) * BP <= n) {
 #pragma unroll
-    for (int k = 0; k <= D; ++k) {
-      if (k < nblk) issue(k, k);
-      cp_async_commit();
+      for (int j = 0; j < U; ++j) {
+        const L c = *reinterpret_cast<const L*>(src + j * 512);
+#pragma unroll
+        for (int e = 0; e < PPL; ++e) m = fmax(m, pt_of(c, e).y);
+      }
+    } else {
+      const long long q0 = b * BP + lane * PPL;
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const L c = *reinterpret_cast<const L*>(src + j * 512);
+#pragma unroll
+        for (int e = 0; e < PPL; ++e)
+          if (q0 + j * 32 * PPL + e < n) m = fmax(m, pt_of(c, e).y);
+      }
     }
-    cp_async_wait<1>();
-    S wcur = block_max(0, 0);  // max y of the block being processed
-    S win[D];                  // win[i] = max y of block k+1+i (NEG past the unit)
-#pragma unroll
-    for (int i = 0; i < D; ++i) win[i] = (i + 1 < D && i + 1 < nblk) ? block_max(i + 1, i + 1) : NEG;
+    return warp_max_fast(m);
+  };
 
-    S runmax = ext_l;          // left anchor: everything before the block
-    S umax = NEG;              // the unit's own points (finalize anchor)
-    S lastx = NEG;             // x of the previous block's last point
-    HoodState hs{0, 1};
-    int s_cur = 0;             // ring slot of block k
-    int s_far = D;             // ring slot of block k + D
-    int s_new = D + 1;         // ring slot of block k + D + 1
+  UnitCur cc{0, 0, 0};
+  seek(cc);
+  if (!(cc.b < cc.e)) return;
+
+  // prologue: sequence blocks 0 .. D in flight (one commit group each);
+  // maxima of blocks 0 .. D-1 (block D's comes with iteration 0)
+  UnitCur ci = cc;
+#pragma unroll
+  for (int s = 0; s <= D; ++s) {
+    if (ci.b < ci.e) issue(ci.b, s);
+    cp_async_commit();
+    advance(ci);
+  }
+  cp_async_wait<1>();
+  UnitCur cf = cc;
+  S wcur = block_max(cf.b, 0);  // max y of the block being processed
+  advance(cf);
+  S win[D];                     // win[i] = max y of sequence block k+1+i
+#pragma unroll
+  for (int i = 0; i + 1 < D; ++i) {
+    win[i] = cf.b < cf.e ? block_max(cf.b, i + 1) : NEG;
+    advance(cf);
+  }
+  win[D - 1] = NEG;
+
+  // per-unit state
+  long long u = 0, ubase = 0, ibase = 0, lim = 0;
+  int inst = 0;
+  S ext_l = NEG, ext_r = NEG;
+  S runmax = NEG;               // left anchor: everything before the block
+  S lastx = NEG;                // x of the previous point (lane 0)
+  HoodState hs{0, 1};
+  bool fresh = true;
+  int s_cur = 0;                // ring slot of sequence block k
+  int s_far = D;                // ring slot of block k + D
+  int s_new = D + 1;            // ring slot of block k + D + 1
 
 #pragma unroll 1
-    for (int k = 0; k < nblk; ++k) {
-      // keep D+1 blocks in flight: issue k+D+1, then block k+D has landed
-      if (k + D + 1 < nblk) issue(k + D + 1, s_new);
-      cp_async_commit();
-      cp_async_wait<1>();
-      const S mfar = (k + D < nblk) ? block_max(k + D, s_far) : NEG;
-      win[D - 1] = mfar;
-      S right = (k + D >= nblk) ? ext_r : NEG;
-#pragma unroll
-      for (int i = 0; i < D; ++i) right = fmax(right, win[i]);
-      const S tau = fmin(runmax, right);
+  while (cc.b < cc.e) {
+    // keep D+1 blocks in flight: issue k+D+1, then block k+D has landed
+    if (ci.b < ci.e) issue(ci.b, s_new);
+    cp_async_commit();
+    advance(ci);
+    cp_async_wait<1>();
+    win[D - 1] = cf.b < cf.e ? block_max(cf.b, s_far) : NEG;
+    advance(cf);
 
-      // the block itself, from this lane's own ring bytes
-      L c[U];
-      {
-        const unsigned char* src = ring + s_cur * BB;
-#pragma unroll
-        for (int j = 0; j < U; ++j) c[j] = *reinterpret_cast<const L*>(src + j * 512);
+    if (fresh) {
+      fresh = false;
+      u = unit_of(cc.r);
+      inst = spi == 1 ? (int)u : (int)u / spi;
+      ibase = (long long)inst * p.L;
+      lim = min(n, ibase + p.L);
+      ubase = cc.b * BP;
+      const long long uend = min(cc.e * BP, lim);
+      // edge anchors: max y of up to EXT points on each side of the unit
+      ext_l = NEG;
+      ext_r = NEG;
+      if (ubase > ibase) {
+        const long long l0 = max(ibase, ubase - EXT);
+        for (long long i = l0 + lane; i < ubase; i += 32) ext_l = fmax(ext_l, gpts[i].y);
+        ext_l = warp_max(ext_l);
+        lastx = lane == 0 ? gpts[ubase - 1].x : NEG;
       }
-      const long long bs = ubase + (long long)k * BP;
-      const bool full = k < nfull;
-      const bool first_has_prev = k > 0 || ubase > ibase;
-      S prow = lastx;
-      if (k == 0 && ubase > ibase && lane == 0) prow = gpts[ubase - 1].x;
-      bool ok = true, any = false;
-      if (full) {
+      if (uend < lim) {
+        const long long r1 = min(min(lim, p.read_lim), uend + EXT);
+        for (long long i = uend + lane; i < r1; i += 32) ext_r = fmax(ext_r, gpts[i].y);
+        ext_r = warp_max(ext_r);
+      }
+      runmax = ext_l;
+      hs = HoodState{0, 1};
+    }
+
+    // right anchor: the unit's next blocks inside the window, then EXT
+    const long long nrem = cc.e - cc.b - 1;
+    S right = ext_r;
 #pragma unroll
-        for (int j = 0; j < U; ++j) {
-          const S x0 = pt_of(c[j], 0).x;
-          const S xl = pt_of(c[j], PPL - 1).x;
-          S px = __shfl_up_sync(0xffffffffu, xl, 1);
-          if (lane == 0) px = (j > 0 || first_has_prev) ? prow : NEG;
-          ok = ok && (x0 > px);
-          if constexpr (PPL == 2) ok = ok && (xl > x0);
-          prow = __shfl_sync(0xffffffffu, xl, 31);
+    for (int i = 0; i < D; ++i)
+      if (i < nrem) right = fmax(right, win[i]);
+    const S tau = fmin(runmax, right);
+
+    // the block itself, from this lane's own ring bytes
+    L c[U];
+    {
+      const unsigned char* src = ring + s_cur * BB;
 #pragma unroll
-          for (int e = 0; e < PPL; ++e) any = any || !(pt_of(c[j], e).y < tau);
+      for (int j = 0; j < U; ++j) c[j] = *reinterpret_cast<const L*>(src + j * 512);
+    }
+    const long long bs = cc.b * BP;
+    const bool full = bs + BP <= n;
+    const bool first_has_prev = bs > ibase;
+    S prow = lastx;
+    bool ok = true;
+    unsigned svm = 0;  // survivors of this lane: bit j * PPL + e
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const S x0 = pt_of(c[j], 0).x;
+        const S xl = pt_of(c[j], PPL - 1).x;
+        S px = __shfl_up_sync(0xffffffffu, xl, 1);
+        if (lane == 0) px = (j > 0 || first_has_prev) ? prow : NEG;
+        ok = ok && (x0 > px);
+        if constexpr (PPL == 2) ok = ok && (xl > x0);
+        prow = __shfl_sync(0xffffffffu, xl, 31);
+#pragma unroll
+        for (int e = 0; e < PPL; ++e) svm |= (pt_of(c[j], e).y < tau ? 0u : 1u) << (j * PPL + e);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const S x0 = pt_of(c[j], 0).x;
+        const S xl = pt_of(c[j], PPL - 1).x;
+        S px = __shfl_up_sync(0xffffffffu, xl, 1);
+        if (lane == 0) px = prow;
+        const long long q0 = bs + (long long)(j * 32 + lane) * PPL;
+        const bool chk = (lane > 0 || j > 0 || first_has_prev) && q0 < lim;
+        ok = ok && (!chk || x0 > px);
+        if constexpr (PPL == 2) ok = ok && (!(q0 + 1 < lim) || xl > x0);
+        prow = __shfl_sync(0xffffffffu, xl, 31);
+#pragma unroll
+        for (int e = 0; e < PPL; ++e)
+          svm |= ((!(pt_of(c[j], e).y < tau) && q0 + e < lim) ? 1u : 0u) << (j * PPL + e);
+      }
+    }
+    if (__any_sync(0xffffffffu, !ok)) report_bad_block<S, U>(gpts, bs, lim, ibase, p.err);
+    lastx = prow;
+    if (p.check_range) range_check_block<S, U>(gpts, bs, lim, p.err);
+
+    if (tau == NEG && __any_sync(0xffffffffu, svm != 0)) {
+      // instance edge: exact per-point anchors from warp max-scans in x order
+      // (rows j, lanes, elements); left = everything before the point,
+      // right = everything after it
+      S lft[U][PPL], yv[U][PPL];
+      S carry = runmax;
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        S t = NEG;
+#pragma unroll
+        for (int e = 0; e < PPL; ++e) {
+          const long long q = bs + (long long)(j * 32 + lane) * PPL + e;
+          yv[j][e] = (full || q < lim) ? pt_of(c[j], e).y : NEG;
+          t = fmax(t, yv[j][e]);
         }
+        const S inc = scan_up_max(t, lane);
+        S ex = __shfl_up_sync(0xffffffffu, inc, 1);
+        S P = lane == 0 ? carry : fmax(carry, ex);
+#pragma unroll
+        for (int e = 0; e < PPL; ++e) {
+          lft[j][e] = P;
+          P = fmax(P, yv[j][e]);
+        }
+        carry = fmax(carry, __shfl_sync(0xffffffffu, inc, 31));
+      }
+      carry = right;
+      svm = 0;
+#pragma unroll
+      for (int j = U - 1; j >= 0; --j) {
+        S t = NEG;
+#pragma unroll
+        for (int e = 0; e < PPL; ++e) t = fmax(t, yv[j][e]);
+        const S inc = scan_down_max(t, lane);
+        S ex = __shfl_down_sync(0xffffffffu, inc, 1);
+        S Q = lane == 31 ? carry : fmax(carry, ex);
+#pragma unroll
+        for (int e = PPL - 1; e >= 0; --e) {
+          const S y = yv[j][e];
+          svm |= ((y != NEG && !(y < fmin(lft[j][e], Q))) ? 1u : 0u) << (j * PPL + e);
+          Q = fmax(Q, y);
+        }
+        carry = fmax(carry, __shfl_sync(0xffffffffu, inc, 0));
+      }
+    }
+
+    if (__any_sync(0xffffffffu, svm != 0)) {
+      // compact the survivors into SB in x order (rows j, lanes, elements)
+      int base = 0;
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        unsigned mk[PPL];
+        int before = 0;
+#pragma unroll
+        for (int e = 0; e < PPL; ++e) {
+          mk[e] = __ballot_sync(0xffffffffu, (svm >> (j * PPL + e)) & 1u);
+          before += __popc(mk[e] & below);
+        }
+        int pos = base + before;
+#pragma unroll
+        for (int e = 0; e < PPL; ++e) {
+          if ((svm >> (j * PPL + e)) & 1u) SB[pos++] = pt_of(c[j], e);
+          base += __popc(mk[e]);
+        }
+      }
+      __syncwarp();
+      if (hs.in_smem && base <= 32 && hs.n + base <= HC) {
+        long long h = hs.n;
+        if (lane == 0) h = fold_linear<V>(SB, base, Hs, h);
+        hs.n = __shfl_sync(0xffffffffu, h, 0);
       } else {
-#pragma unroll
-        for (int j = 0; j < U; ++j) {
-          const S x0 = pt_of(c[j], 0).x;
-          const S xl = pt_of(c[j], PPL - 1).x;
-          S px = __shfl_up_sync(0xffffffffu, xl, 1);
-          if (lane == 0) px = prow;
-          const long long q0 = bs + (long long)(j * 32 + lane) * PPL;
-          const bool chk = (lane > 0 || j > 0 || first_has_prev) && q0 < lim;
-          ok = ok && (!chk || x0 > px);
-          if constexpr (PPL == 2) ok = ok && (!(q0 + 1 < lim) || xl > x0);
-          prow = __shfl_sync(0xffffffffu, xl, 31);
-#pragma unroll
-          for (int e = 0; e < PPL; ++e) any = any || (!(pt_of(c[j], e).y < tau) && q0 + e < lim);
-        }
+        hs = merge_block_tree<S, HC>(SB, base, mns, mnc, Hs, gout + ubase, hs);
       }
-      if (__any_sync(0xffffffffu, !ok)) report_bad_block<S, U>(gpts, bs, lim, ibase, p.err);
-      lastx = prow;
-      if (p.check_range) range_check_block<S, U>(gpts, bs, lim, p.err);
+      __syncwarp();
+    }
+    runmax = fmax(runmax, wcur);
+    // slide the window: the block after this one becomes current
+    wcur = win[0];
+#pragma unroll
+    for (int i = 0; i + 1 < D; ++i) win[i] = win[i + 1];
+    s_cur = (s_cur + 1 == R) ? 0 : s_cur + 1;
+    s_far = (s_far + 1 == R) ? 0 : s_far + 1;
+    s_new = (s_new + 1 == R) ? 0 : s_new + 1;
 
-      if (__any_sync(0xffffffffu, any)) {
-        // compact the survivors into SB in x order (rows j, lanes, elements)
-        int base = 0;
-#pragma unroll
-        for (int j = 0; j < U; ++j) {
-          bool sv[PPL];
-          unsigned mk[PPL];
-          int before = 0;
-#pragma unroll
-          for (int e = 0; e < PPL; ++e) {
-            const long long q = bs + (long long)(j * 32 + lane) * PPL + e;
-            sv[e] = !(pt_of(c[j], e).y < tau) && (full || q < lim);
-            mk[e] = __ballot_sync(0xffffffffu, sv[e]);
-            before += __popc(mk[e] & below);
-          }
-          int pos = base + before;
-#pragma unroll
-          for (int e = 0; e < PPL; ++e) {
-            if (sv[e]) SB[pos++] = pt_of(c[j], e);
-            base += __popc(mk[e]);
+    if (nrem == 0) {
+      // unit done: its hood to the output slots, its summary for finalize
+      if (hs.in_smem)
+        for (long long e = lane; e < hs.n; e += 32) gout[ubase + e] = Hs[e];
+      if (spi > 1) {
+        // anchor point for finalize: the unit's highest hood corner (a real
+        // input point; y along a hood is unimodal, so a spilled hood is searched)
+        V apt = make_vec<V>(NEG, NEG);
+        if (hs.n > 0) {
+          if (hs.in_smem) {
+            for (long long e = lane; e < hs.n; e += 32)
+              if (Hs[e].y > apt.y) apt = Hs[e];
+            apt = warp_argmax_y(apt);
+          } else if (lane == 0) {
+            const V* h = gout + ubase;
+            long long a = 0, b = hs.n - 1;
+            while (a < b) {
+              const long long mid = (a + b) >> 1;
+              if (h[mid + 1].y > h[mid].y) a = mid + 1;
+              else b = mid;
+            }
+            apt = h[a];
           }
         }
-        __syncwarp();
-        if (hs.in_smem && base <= 32 && hs.n + base <= HC) {
-          long long h = hs.n;
-          if (lane == 0) h = fold_linear<V>(SB, base, Hs, h);
-          hs.n = __shfl_sync(0xffffffffu, h, 0);
+        if (lane == 0) reinterpret_cast<V*>(p.seg_apt)[u] = apt;
+      }
+      if (lane == 0) {
+        if (spi == 1) {
+          p.out_counts[inst] = (int)hs.n;
         } else {
-          hs = merge_block_tree<S, HC>(SB, base, mns, mnc, Hs, gout + ubase, hs);
-        }
-        __syncwarp();
-      }
-      umax = fmax(umax, wcur);
-      runmax = fmax(runmax, wcur);
-      // slide the window: the block after this one becomes current
-      wcur = win[0];
-#pragma unroll
-      for (int i = 0; i + 1 < D; ++i) win[i] = win[i + 1];
-      s_cur = (s_cur + 1 == R) ? 0 : s_cur + 1;
-      s_far = (s_far + 1 == R) ? 0 : s_far + 1;
-      s_new = (s_new + 1 == R) ? 0 : s_new + 1;
-    }
-    cp_async_wait<0>();
-    __syncwarp();
-    (void)umax;
-
-    if (hs.in_smem)
-      for (long long e = lane; e < hs.n; e += 32) gout[ubase + e] = Hs[e];
-    if (spi > 1) {
-      // anchor point for finalize: the unit's highest hood corner (a real
-      // input point; y along a hood is unimodal, so a spilled hood is searched)
-      V apt = make_vec<V>(NEG, NEG);
-      if (hs.n > 0) {
-        if (hs.in_smem) {
-          for (long long e = lane; e < hs.n; e += 32)
-            if (Hs[e].y > apt.y) apt = Hs[e];
-          apt = warp_argmax_y(apt);
-        } else if (lane == 0) {
-          const V* h = gout + ubase;
-          long long a = 0, b = hs.n - 1;
-          while (a < b) {
-            const long long mid = (a + b) >> 1;
-            if (h[mid + 1].y > h[mid].y) a = mid + 1;
-            else b = mid;
-          }
-          apt = h[a];
+          p.seg_cnt[u] = (int)hs.n;
+          p.seg_base[u] = ubase;
         }
       }
-      if (lane == 0) reinterpret_cast<V*>(p.seg_apt)[u] = apt;
+      __syncwarp();
+      fresh = true;
     }
-    if (lane == 0) {
-      if (spi == 1) {
-        p.out_counts[inst] = (int)hs.n;
-      } else {
-        p.seg_cnt[u] = (int)hs.n;
-        p.seg_base[u] = ubase;
-      }
-    }
-    __syncwarp();
+    advance(cc);
   }
+  cp_async_wait<0>();
 }
 
 // ------------------------------------------------------------ instance kernel
