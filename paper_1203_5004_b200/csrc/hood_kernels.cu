@@ -597,20 +597,22 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// Per-warp shared memory of the ring kernel.
-template <class S, int D>
+// Per-warp shared memory of the ring kernel: R = D + P + 1 block slots (the
+// block being processed, D landed blocks of lookahead, P blocks in flight),
+// the unit's running hood and a small buffer of pending survivors.
+template <class S, int D, int P>
 struct RingLayout {
   using V = typename PointT<S>::V;
   static constexpr size_t up(size_t x, size_t a) { return (x + a - 1) / a * a; }
-  static constexpr int U = 4;                                           // 16-byte units per lane per block
-  static constexpr int R = D + 2;                                       // ring slots
+  static constexpr int U = 4;                                           // 16-byte chunks per lane per block
+  static constexpr int R = D + P + 1;                                   // ring slots
   static constexpr int BP = 32 * U * Ld16<S>::PPL;                      // points per block
-  static constexpr size_t BB = 32 * U * 16;                             // bytes per block (2 KB)
-  static constexpr size_t RING = 0;                                     // [R] blocks, lane-interleaved
-  static constexpr size_t BM = RING + (size_t)R * BB;                   // [R] block maxima
-  static constexpr size_t SB = up(BM + (size_t)R * sizeof(S), 16);      // [BP] block survivors
-  static constexpr size_t HS = SB + (size_t)BP * sizeof(V);             // [HC] running unit hood
-  static constexpr size_t MNS = up(HS + (size_t)HCap<S>::value * sizeof(V), 8);  // [32] tree starts
+  static constexpr size_t BB = 32 * U * 16;                             // bytes per block
+  static constexpr int PC = 64;                                         // pending survivor capacity
+  static constexpr size_t RING = 0;                                     // [R] blocks
+  static constexpr size_t HS = RING + (size_t)R * BB;                   // [HC] running unit hood
+  static constexpr size_t PB = HS + (size_t)HCap<S>::value * sizeof(V); // [PC] pending survivors
+  static constexpr size_t MNS = up(PB + (size_t)PC * sizeof(V), 8);     // [32] tree starts
   static constexpr size_t MNC = MNS + 32 * 8;                           // [32] tree counts
   static constexpr size_t BYTES = up(MNC + 32 * 4, 128);
 };
@@ -635,54 +637,169 @@ __device__ __forceinline__ S scan_down_max(S v, int lane) {
   return v;
 }
 
+__device__ __forceinline__ void cp_async16s(unsigned dst, const void* gsrc, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(gsrc), "r"(src_bytes) : "memory");
+}
+template <class L>
+__device__ __forceinline__ L lds16(unsigned a);
+template <>
+__device__ __forceinline__ float4 lds16<float4>(unsigned a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+template <>
+__device__ __forceinline__ double2 lds16<double2>(unsigned a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ float2 lds_pt(unsigned a, float2*) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ double2 lds_pt(unsigned a, double2*) { return lds16<double2>(a); }
+
+// Survivors of a block at an instance edge (lane bit i: point i of the lane's
+// run, smem run address a, first global index q0): exact per-point anchors
+// on the side(s) without a block anchor -- left = max y of everything before
+// the point (runmax == -inf), right = of everything after it (right == -inf).
+template <class S, int U>
+__device__ __noinline__ unsigned edge_survivors(unsigned a, long long q0, long long n, S runmax, S right) {
+  using L = typename Ld16<S>::T;
+  constexpr int PPL = Ld16<S>::PPL, NP = U * PPL;
+  constexpr unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const S NEG = neg_inf<S>();
+  L c[U];
+#pragma unroll
+  for (int k = 0; k < U; ++k) c[k] = lds16<L>(a ^ (k << 4));
+  S yv[NP];
+  S t = NEG;
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    yv[i] = (q0 + i < n) ? pt_of(c[i / PPL], i % PPL).y : NEG;
+    t = fmax(t, yv[i]);
+  }
+  S lft[NP];
+  if (runmax == NEG) {
+    const S incl = scan_up_max(t, lane);
+    S P0 = __shfl_up_sync(FULL, incl, 1);
+    P0 = lane == 0 ? NEG : P0;
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      lft[i] = P0;
+      P0 = fmax(P0, yv[i]);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NP; ++i) lft[i] = runmax;
+  }
+  unsigned svm = 0;
+  if (right == NEG) {
+    const S incr = scan_down_max(t, lane);
+    S Q = __shfl_down_sync(FULL, incr, 1);
+    Q = lane == 31 ? NEG : Q;
+#pragma unroll
+    for (int i = NP - 1; i >= 0; --i) {
+      const S y = yv[i];
+      svm |= ((y != NEG && !(y < fmin(lft[i], Q))) ? 1u : 0u) << i;
+      Q = fmax(Q, y);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      const S y = yv[i];
+      svm |= ((y != NEG && !(y < fmin(lft[i], right))) ? 1u : 0u) << i;
+    }
+  }
+  return svm;
+}
+
+#ifndef HOOD_RING_MAXNREG
+#define HOOD_RING_MAXNREG 168
+#endif
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 // Position of one warp in its sequence of units: the unit with serial r
 // (u = unit_lo + gw + r * nwarps) and the block range [b, e) still ahead of
 // the cursor (global block indices).  Past the last unit b >= e.
 struct UnitCur {
-  int r;
-  long long b, e;
+  int r, b, e;
 };
+
+// Lane l owns the l-th run of U 16-byte chunks of a block (consecutive in x);
+// its chunk k sits at byte  l*16U + ((k ^ rot(l)) * 16)  of the slot, so both
+// the scattered cp.async writes and the 16-byte reads of a quarter warp hit
+// eight distinct bank groups.
+template <int U>
+__device__ __forceinline__ int ring_rot(int l) {
+  return U == 8 ? (l & 7) : ((l >> 1) & 3);
+}
 
 // The hot kernel.  Every warp is an independent pipeline over its own
 // sequence of units (contiguous x-ranges of the input; a whole instance in
-// batched builds).  Its lanes stream the blocks (2 KB: 256 float2 / 128 double2
-// points) of that sequence with coalesced 16-byte cp.async into a per-warp
-// ring of R = D + 2 smem slots, D blocks ahead of the block being processed --
-// across unit boundaries, so short units (batched instances) never drain the
-// pipeline.  A block's maximum y is taken when it lands; the block itself is
-// processed D iterations later with
-//   left  = max y of the unit's earlier blocks (or of the EXT points before
-//           the unit),
-//   right = max y of the unit's next (up to D) blocks and of the EXT points
-//           after the unit,
-// both sets strictly left / right of every point of the block: a point below
-// min(left, right) lies strictly below the chord of two input points that
-// straddle it, cannot be a corner of the final hood (oracle.cpp:7-20 pops it)
-// and is dropped with one compare.  A block at an instance edge (no point on
-// one side) gets exact per-point anchors instead: warp max-scans over the block
-// in x order.  The rare survivors are compacted in x order with ballots and
-// folded into the unit's running hood (monotone-chain pushes, or a warp merge
-// tree + bridge -- kernel.hpp:31-67 -- when many).  x strictly increasing is
-// checked on the way (validate_points, hoodbuf.cpp:48-58).  Lanes only ever
-// read the smem bytes they copied themselves, so no barrier of any kind is
-// needed.
-template <class S, int D>
-__global__ void __launch_bounds__(128) ring_hull_kernel(const SlabParams<S> p) {
+// batched builds).  Its lanes stream the blocks of that sequence (256 float2 /
+// 128 double2 points) with coalesced 16-byte cp.async into a per-warp ring of
+// smem slots, P blocks in flight and D landed blocks of lookahead ahead of the
+// block being processed -- across unit boundaries, so short units (batched
+// instances) never drain the pipeline.
+//   Landing (once per block, from smem): each lane takes the maximum y of its
+//   run and checks x strictly increasing (validate_points, hoodbuf.cpp:48-58);
+//   the warp maximum is the block's anchor value.
+//   Processing, D blocks later, with
+//     left  = max y of the unit's earlier blocks (or of the EXT points before
+//             the unit),
+//     right = max y of the unit's next (up to D) blocks and of the EXT points
+//             after the unit:
+//   a point below tau = min(left, right) lies strictly below the chord of two
+//   input points that straddle it, cannot be a corner of the final hood
+//   (oracle.cpp:7-20 pops it) and is dropped -- for a whole lane run with one
+//   compare of the run's maximum.  The rare runs that reach tau are re-read
+//   point-per-lane and their survivors queued; queued survivors are folded
+//   into the unit's running hood by monotone-chain pushes (or a warp merge
+//   tree + bridge, kernel.hpp:31-67, when many).  A block at an instance edge
+//   (no anchor on one side) gets exact per-point anchors from warp max-scans.
+// Every warp touches only its own smem, so no CTA barrier is ever needed.
+template <class S, int D, int P>
+__global__ void __maxnreg__(HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams<S> p) {
   using V = typename PointT<S>::V;
   using L = typename Ld16<S>::T;
-  using LY = RingLayout<S, D>;
+  using LY = RingLayout<S, D, P>;
   constexpr int U = LY::U, R = LY::R, PPL = Ld16<S>::PPL;
+  constexpr int NP = U * PPL;  // points per lane run
   constexpr int BP = LY::BP;
   constexpr int BB = (int)LY::BB;
   constexpr int HC = HCap<S>::value;
+  constexpr int PC = LY::PC;
   constexpr int EXT = 128;
+  constexpr unsigned FULL = 0xffffffffu;
+  static_assert(U == 4 || U == 8, "ring swizzle");
+  static_assert(NP <= PC && NP <= 32, "pending buffer");
 
   extern __shared__ unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned char* wb = smem_raw + (size_t)warp * LY::BYTES;
-  unsigned char* ring = wb + LY::RING + lane * 16;  // this lane's column of the ring
-  V* SB = reinterpret_cast<V*>(wb + LY::SB);
+  const unsigned pad = (128u - (smem_u32(smem_raw) & 127u)) & 127u;
+  unsigned char* wb = smem_raw + pad + (size_t)warp * LY::BYTES;
+  const unsigned ring_s = smem_u32(wb + LY::RING);
+  // cp.async destination of the lane's chunk in copy j: wr + j*512 (U == 4),
+  // (wr + j*512) ^ ((j & 1) << 6) (U == 8)
+  const unsigned wr = U == 8 ? ring_s + (lane >> 3) * 128 + (((lane & 7) ^ (lane >> 3)) << 4)
+                             : ring_s + (lane >> 2) * 64 + (((lane & 3) ^ ((lane >> 3) & 3)) << 4);
+  auto run_addr = [&](int l, int slot) -> unsigned {
+    return ring_s + slot * BB + l * (16 * U) + (ring_rot<U>(l) << 4);
+  };
   V* Hs = reinterpret_cast<V*>(wb + LY::HS);
+  V* PBf = reinterpret_cast<V*>(wb + LY::PB);
   long long* mns = reinterpret_cast<long long*>(wb + LY::MNS);
   int* mnc = reinterpret_cast<int*>(wb + LY::MNC);
   const V* gpts = reinterpret_cast<const V*>(p.pts);
@@ -692,130 +809,206 @@ __global__ void __launch_bounds__(128) ring_hull_kernel(const SlabParams<S> p) {
   const unsigned below = (1u << lane) - 1u;
 
   const int spi = p.slabs_per_inst;
-  const long long bpi = p.tiles_per_inst;  // blocks per instance
+  const int bpi = (int)p.tiles_per_inst;  // blocks per instance
   const long long n = p.n;
   const long long n_bytes = n * (long long)sizeof(V);
-  const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
-  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  const int nfull = (int)(n / BP);        // blocks [0, nfull) are full
+  const int gw = blockIdx.x * (blockDim.x >> 5) + warp;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
 
-  auto unit_of = [&](int r) -> long long { return p.unit_lo + gw + (long long)r * nwarps; };
   auto seek = [&](UnitCur& c) {  // c.r set: load the block range of its unit
-    const long long u = unit_of(c.r);
+    const long long u = p.unit_lo + gw + (long long)c.r * nwarps;
     if (u < p.unit_hi) {
       if (spi == 1) {
-        c.b = u * bpi;
+        c.b = (int)u * bpi;
         c.e = c.b + bpi;
       } else {
         const int uu = (int)u, inst = uu / spi, js = uu - inst * spi;
-        c.b = (long long)inst * bpi + ((long long)js * bpi) / spi;
-        c.e = (long long)inst * bpi + ((long long)(js + 1) * bpi) / spi;
+        c.b = inst * bpi + (int)(((long long)js * bpi) / spi);
+        c.e = inst * bpi + (int)(((long long)(js + 1) * bpi) / spi);
       }
     } else {
       c.b = c.e = 0;
     }
   };
-  auto advance = [&](UnitCur& c) {
+  // returns true when the cursor moved into a new unit
+  auto advance = [&](UnitCur& c) -> bool {
     if (c.b < c.e && ++c.b == c.e) {
       ++c.r;
       seek(c);
+      return true;
     }
+    return false;
   };
-  // copy global block b into ring slot s (lane column); the input's last
-  // block is clamped (cp.async zero-fills the rest)
-  auto issue = [&](long long b, int s) {
-    const long long off = b * (long long)BB;
-    unsigned char* dst = ring + s * BB;
-    if ((b + 1) * BP <= n) {
+  // copy global block b into ring slot s; the input's last block is clamped
+  // (cp.async zero-fills the rest)
+  auto issue = [&](int b, int s) {
+    const long long off = (long long)b * BB;
+    const unsigned dst = wr + s * BB;
+    if (b < nfull) {
 #pragma unroll
-      for (int j = 0; j < U; ++j) cp_async16(dst + j * 512, gbytes + off + j * 512, 16);
+      for (int j = 0; j < U; ++j) cp_async16s((dst + j * 512) ^ (U == 8 ? (j & 1) << 6 : 0), gbytes + off + j * 512, 16);
     } else {
 #pragma unroll
       for (int j = 0; j < U; ++j) {
         const long long rem = n_bytes - (off + lane * 16 + j * 512);
         const int nb = rem >= 16 ? 16 : (rem > 0 ? (int)rem : 0);
-        cp_async16(dst + j * 512, nb ? gbytes + off + j * 512 : gbytes, nb);
+        cp_async16s((dst + j * 512) ^ (U == 8 ? (j & 1) << 6 : 0), nb ? gbytes + off + j * 512 : gbytes, nb);
       }
     }
   };
-  // max y of global block b (slot s) over the warp; missing points masked
-  auto block_max = [&](long long b, int s) -> S {
-    const unsigned char* src = ring + s * BB;
-    S m = NEG;
-    if ((b + 1) * BP <= n) {
+  // first error of block b (slow path): rescan it from global memory
+  auto report = [&](int b, bool range) {
+    const long long inst = b / bpi;
+    const long long ib = inst * p.L, lm = min(n, ib + p.L);
+    if (range) range_check_block<S, U>(gpts, (long long)b * BP, lm, p.err);
+    else report_bad_block<S, U>(gpts, (long long)b * BP, lm, ib, p.err);
+  };
+  // landing pass over global block b in slot s: the lane's run maximum y,
+  // x strictly increasing (xc: x of the point before the block, used by lane 0
+  // when has_pred); xc becomes the block's last x
+  auto land = [&](int b, int s, bool has_pred, S& xc) -> S {
+    L c[U];
+    const unsigned a = run_addr(lane, s);
 #pragma unroll
-      for (int j = 0; j < U; ++j) {
-        const L c = *reinterpret_cast<const L*>(src + j * 512);
+    for (int k = 0; k < U; ++k) c[k] = lds16<L>(a ^ (k << 4));
+    const S xl = pt_of(c[U - 1], PPL - 1).x;
+    S prev = __shfl_up_sync(FULL, xl, 1);
+    if (lane == 0) prev = has_pred ? xc : NEG;
+    S m0 = NEG, m1 = NEG;
+    bool ok = true;
+    if (b < nfull) {
 #pragma unroll
-        for (int e = 0; e < PPL; ++e) m = fmax(m, pt_of(c, e).y);
-      }
+      for (int k = 0; k < U; ++k)
+#pragma unroll
+        for (int e = 0; e < PPL; ++e) {
+          const V q = pt_of(c[k], e);
+          ok = ok && (q.x > prev);
+          prev = q.x;
+          if ((k * PPL + e) & 1) m1 = fmax(m1, q.y);
+          else m0 = fmax(m0, q.y);
+        }
     } else {
-      const long long q0 = b * BP + lane * PPL;
+      const long long q0 = (long long)b * BP + lane * NP;
 #pragma unroll
-      for (int j = 0; j < U; ++j) {
-        const L c = *reinterpret_cast<const L*>(src + j * 512);
+      for (int k = 0; k < U; ++k)
 #pragma unroll
-        for (int e = 0; e < PPL; ++e)
-          if (q0 + j * 32 * PPL + e < n) m = fmax(m, pt_of(c, e).y);
-      }
+        for (int e = 0; e < PPL; ++e) {
+          const V q = pt_of(c[k], e);
+          const bool valid = q0 + k * PPL + e < n;
+          ok = ok && (!valid || q.x > prev);
+          prev = q.x;
+          if (valid) m0 = fmax(m0, q.y);
+        }
     }
-    return warp_max_fast(m);
+    if (p.check_range) {
+      const long long q0 = (long long)b * BP + lane * NP;
+      bool in = true;
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+#pragma unroll
+        for (int e = 0; e < PPL; ++e) {
+          const S x = pt_of(c[k], e).x;
+          in = in && (!(q0 + k * PPL + e < n) || (x > (S)0 && x < (S)1));
+        }
+      if (__any_sync(FULL, !in)) report(b, true);
+    }
+    xc = __shfl_sync(FULL, xl, 31);
+    if (__any_sync(FULL, !ok)) report(b, false);
+    return fmax(m0, m1);
   };
 
+  // profiling (p.trace, globaltimer ns): [0] first warp entry, [1] last warp
+  // exit, [2] last prologue end; per warp gw at [1024 + 4 gw]: entry, exit, SM
+  if (p.trace && lane == 0) atomicMin(reinterpret_cast<unsigned long long*>(p.trace), gtimer());
+  if (p.trace && lane == 0) p.trace[1024 + 4 * gw] = (long long)gtimer();
   UnitCur cc{0, 0, 0};
   seek(cc);
   if (!(cc.b < cc.e)) return;
 
-  // prologue: sequence blocks 0 .. D in flight (one commit group each);
-  // maxima of blocks 0 .. D-1 (block D's comes with iteration 0)
+  // prologue: sequence blocks 0 .. D+P-1 in flight (one commit group each),
+  // then blocks 0 .. D-1 landed
   UnitCur ci = cc;
-#pragma unroll
-  for (int s = 0; s <= D; ++s) {
+#pragma unroll 1
+  for (int s = 0; s < D + P; ++s) {
     if (ci.b < ci.e) issue(ci.b, s);
     cp_async_commit();
     advance(ci);
   }
-  cp_async_wait<1>();
+  cp_async_wait<P>();
+  __syncwarp();
   UnitCur cf = cc;
-  S wcur = block_max(cf.b, 0);  // max y of the block being processed
-  advance(cf);
-  S win[D];                     // win[i] = max y of sequence block k+1+i
+  bool cf_first = true;  // the next block to land starts its unit
+  S xcf = NEG;           // x of the point before the next block to land
+  S lmw[D], win[D];      // lane run / block maxima of sequence blocks k+1 .. k+D
+  S lmc, wcur;           // ... of block k
+  auto land_next = [&](int slot, S& lm, S& bm) {
+    if (cf.b < cf.e) {
+      bool hp = true;
+      if (cf_first) {
+        hp = (cf.b % bpi) != 0;
+        xcf = hp ? gpts[(long long)cf.b * BP - 1].x : NEG;
+      }
+      lm = land(cf.b, slot, hp, xcf);
+      bm = warp_max_fast(lm);
+    } else {
+      lm = NEG;
+      bm = NEG;
+    }
+    cf_first = advance(cf);
+  };
+  land_next(0, lmc, wcur);
 #pragma unroll
-  for (int i = 0; i + 1 < D; ++i) {
-    win[i] = cf.b < cf.e ? block_max(cf.b, i + 1) : NEG;
-    advance(cf);
-  }
+  for (int i = 0; i + 1 < D; ++i) land_next(i + 1, lmw[i], win[i]);
+  lmw[D - 1] = NEG;
   win[D - 1] = NEG;
+  if (p.trace && lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(p.trace) + 2, gtimer());
 
   // per-unit state
-  long long u = 0, ubase = 0, ibase = 0, lim = 0;
+  long long u = 0, ubase = 0;
   int inst = 0;
   S ext_l = NEG, ext_r = NEG;
-  S runmax = NEG;               // left anchor: everything before the block
-  S lastx = NEG;                // x of the previous point (lane 0)
+  S runmax = NEG;   // left anchor: everything before the block
   HoodState hs{0, 1};
+  int pend = 0;     // queued survivors in PBf
   bool fresh = true;
-  int s_cur = 0;                // ring slot of sequence block k
-  int s_far = D;                // ring slot of block k + D
-  int s_new = D + 1;            // ring slot of block k + D + 1
+  int s_cur = 0;    // ring slot of sequence block k
+  int s_far = D;    // ring slot of block k + D
+  int s_new = D + P;  // ring slot of block k + D + P
+
+  // fold the queued survivors (x order) into the running hood
+  auto flush = [&]() {
+    __syncwarp();
+    if (pend == 0) return;
+    if (hs.in_smem && pend <= 32 && hs.n + pend <= HC) {
+      long long h = hs.n;
+      if (lane == 0) h = fold_linear<V>(PBf, pend, Hs, h);
+      hs.n = __shfl_sync(FULL, h, 0);
+    } else {
+      hs = merge_block_tree<S, HC>(PBf, pend, mns, mnc, Hs, gout + ubase, hs);
+    }
+    pend = 0;
+    __syncwarp();
+  };
 
 #pragma unroll 1
   while (cc.b < cc.e) {
-    // keep D+1 blocks in flight: issue k+D+1, then block k+D has landed
+    // keep P blocks in flight: issue k+D+P, then block k+D has landed
     if (ci.b < ci.e) issue(ci.b, s_new);
     cp_async_commit();
     advance(ci);
-    cp_async_wait<1>();
-    win[D - 1] = cf.b < cf.e ? block_max(cf.b, s_far) : NEG;
-    advance(cf);
+    cp_async_wait<P>();
+    __syncwarp();  // the landed block was copied by all lanes
+    land_next(s_far, lmw[D - 1], win[D - 1]);
 
     if (fresh) {
       fresh = false;
-      u = unit_of(cc.r);
+      u = p.unit_lo + gw + (long long)cc.r * nwarps;
       inst = spi == 1 ? (int)u : (int)u / spi;
-      ibase = (long long)inst * p.L;
-      lim = min(n, ibase + p.L);
-      ubase = cc.b * BP;
-      const long long uend = min(cc.e * BP, lim);
+      const long long ibase = (long long)inst * p.L;
+      const long long lim = min(n, ibase + p.L);
+      ubase = (long long)cc.b * BP;
+      const long long uend = min((long long)cc.e * BP, lim);
       // edge anchors: max y of up to EXT points on each side of the unit
       ext_l = NEG;
       ext_r = NEG;
@@ -823,7 +1016,6 @@ __global__ void __launch_bounds__(128) ring_hull_kernel(const SlabParams<S> p) {
         const long long l0 = max(ibase, ubase - EXT);
         for (long long i = l0 + lane; i < ubase; i += 32) ext_l = fmax(ext_l, gpts[i].y);
         ext_l = warp_max(ext_l);
-        lastx = lane == 0 ? gpts[ubase - 1].x : NEG;
       }
       if (uend < lim) {
         const long long r1 = min(min(lim, p.read_lim), uend + EXT);
@@ -832,148 +1024,101 @@ __global__ void __launch_bounds__(128) ring_hull_kernel(const SlabParams<S> p) {
       }
       runmax = ext_l;
       hs = HoodState{0, 1};
+      pend = 0;
     }
 
     // right anchor: the unit's next blocks inside the window, then EXT
-    const long long nrem = cc.e - cc.b - 1;
+    const int nrem = cc.e - cc.b - 1;
     S right = ext_r;
 #pragma unroll
     for (int i = 0; i < D; ++i)
       if (i < nrem) right = fmax(right, win[i]);
     const S tau = fmin(runmax, right);
+    const long long bs = (long long)cc.b * BP;
 
-    // the block itself, from this lane's own ring bytes
-    L c[U];
-    {
-      const unsigned char* src = ring + s_cur * BB;
-#pragma unroll
-      for (int j = 0; j < U; ++j) c[j] = *reinterpret_cast<const L*>(src + j * 512);
-    }
-    const long long bs = cc.b * BP;
-    const bool full = bs + BP <= n;
-    const bool first_has_prev = bs > ibase;
-    S prow = lastx;
-    bool ok = true;
-    unsigned svm = 0;  // survivors of this lane: bit j * PPL + e
-    if (full) {
-#pragma unroll
-      for (int j = 0; j < U; ++j) {
-        const S x0 = pt_of(c[j], 0).x;
-        const S xl = pt_of(c[j], PPL - 1).x;
-        S px = __shfl_up_sync(0xffffffffu, xl, 1);
-        if (lane == 0) px = (j > 0 || first_has_prev) ? prow : NEG;
-        ok = ok && (x0 > px);
-        if constexpr (PPL == 2) ok = ok && (xl > x0);
-        prow = __shfl_sync(0xffffffffu, xl, 31);
-#pragma unroll
-        for (int e = 0; e < PPL; ++e) svm |= (pt_of(c[j], e).y < tau ? 0u : 1u) << (j * PPL + e);
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < U; ++j) {
-        const S x0 = pt_of(c[j], 0).x;
-        const S xl = pt_of(c[j], PPL - 1).x;
-        S px = __shfl_up_sync(0xffffffffu, xl, 1);
-        if (lane == 0) px = prow;
-        const long long q0 = bs + (long long)(j * 32 + lane) * PPL;
-        const bool chk = (lane > 0 || j > 0 || first_has_prev) && q0 < lim;
-        ok = ok && (!chk || x0 > px);
-        if constexpr (PPL == 2) ok = ok && (!(q0 + 1 < lim) || xl > x0);
-        prow = __shfl_sync(0xffffffffu, xl, 31);
-#pragma unroll
-        for (int e = 0; e < PPL; ++e)
-          svm |= ((!(pt_of(c[j], e).y < tau) && q0 + e < lim) ? 1u : 0u) << (j * PPL + e);
-      }
-    }
-    if (__any_sync(0xffffffffu, !ok)) report_bad_block<S, U>(gpts, bs, lim, ibase, p.err);
-    lastx = prow;
-    if (p.check_range) range_check_block<S, U>(gpts, bs, lim, p.err);
-
-    if (tau == NEG && __any_sync(0xffffffffu, svm != 0)) {
-      // instance edge: exact per-point anchors from warp max-scans in x order
-      // (rows j, lanes, elements); left = everything before the point,
-      // right = everything after it
-      S lft[U][PPL], yv[U][PPL];
-      S carry = runmax;
-#pragma unroll
-      for (int j = 0; j < U; ++j) {
-        S t = NEG;
-#pragma unroll
-        for (int e = 0; e < PPL; ++e) {
-          const long long q = bs + (long long)(j * 32 + lane) * PPL + e;
-          yv[j][e] = (full || q < lim) ? pt_of(c[j], e).y : NEG;
-          t = fmax(t, yv[j][e]);
+    // lane runs reaching tau (every run at an instance edge)
+    const unsigned cm = tau != NEG ? __ballot_sync(FULL, !(lmc < tau)) : FULL;
+    if (cm != 0 && cm != FULL && __popc(cm) <= 2) {
+      // a few runs: re-read them point-per-lane, queue the survivors
+      unsigned cr = cm;
+      while (cr) {
+        const int cl = __ffs(cr) - 1;
+        cr &= cr - 1;
+        V q = make_vec<V>(NEG, NEG);
+        bool sv = false;
+        if (lane < NP) {
+          const unsigned a = (run_addr(cl, s_cur) ^ ((lane / PPL) << 4)) + (lane % PPL) * (unsigned)sizeof(V);
+          q = lds_pt(a, (V*)nullptr);
+          sv = (bs + cl * NP + lane < n) && !(q.y < tau);
         }
-        const S inc = scan_up_max(t, lane);
-        S ex = __shfl_up_sync(0xffffffffu, inc, 1);
-        S P = lane == 0 ? carry : fmax(carry, ex);
-#pragma unroll
-        for (int e = 0; e < PPL; ++e) {
-          lft[j][e] = P;
-          P = fmax(P, yv[j][e]);
-        }
-        carry = fmax(carry, __shfl_sync(0xffffffffu, inc, 31));
+        const unsigned sm = __ballot_sync(FULL, sv);
+        const int cnt = __popc(sm);
+        if (pend + cnt > PC) flush();
+        if (sv) PBf[pend + __popc(sm & below)] = q;
+        pend += cnt;
       }
-      carry = right;
-      svm = 0;
+    } else if (cm != 0) {
+      // many runs (arc-like input) or an instance edge (exact per-point
+      // anchors on the side(s) without a block anchor): the whole block
+      unsigned svm;
+      L c[U];
+      {
+        const unsigned a = run_addr(lane, s_cur);
+        if (tau == NEG) svm = edge_survivors<S, U>(a, bs + lane * NP, n, runmax, right);
 #pragma unroll
-      for (int j = U - 1; j >= 0; --j) {
-        S t = NEG;
-#pragma unroll
-        for (int e = 0; e < PPL; ++e) t = fmax(t, yv[j][e]);
-        const S inc = scan_down_max(t, lane);
-        S ex = __shfl_down_sync(0xffffffffu, inc, 1);
-        S Q = lane == 31 ? carry : fmax(carry, ex);
-#pragma unroll
-        for (int e = PPL - 1; e >= 0; --e) {
-          const S y = yv[j][e];
-          svm |= ((y != NEG && !(y < fmin(lft[j][e], Q))) ? 1u : 0u) << (j * PPL + e);
-          Q = fmax(Q, y);
-        }
-        carry = fmax(carry, __shfl_sync(0xffffffffu, inc, 0));
+        for (int k = 0; k < U; ++k) c[k] = lds16<L>(a ^ (k << 4));
       }
-    }
-
-    if (__any_sync(0xffffffffu, svm != 0)) {
-      // compact the survivors into SB in x order (rows j, lanes, elements)
-      int base = 0;
+      if (tau != NEG) {
+        const long long q0 = bs + lane * NP;
+        svm = 0;
 #pragma unroll
-      for (int j = 0; j < U; ++j) {
-        unsigned mk[PPL];
-        int before = 0;
-#pragma unroll
-        for (int e = 0; e < PPL; ++e) {
-          mk[e] = __ballot_sync(0xffffffffu, (svm >> (j * PPL + e)) & 1u);
-          before += __popc(mk[e] & below);
-        }
-        int pos = base + before;
-#pragma unroll
-        for (int e = 0; e < PPL; ++e) {
-          if ((svm >> (j * PPL + e)) & 1u) SB[pos++] = pt_of(c[j], e);
-          base += __popc(mk[e]);
-        }
+        for (int i = 0; i < NP; ++i)
+          svm |= ((q0 + i < n) && !(pt_of(c[i / PPL], i % PPL).y < tau) ? 1u : 0u) << i;
       }
-      __syncwarp();
-      if (hs.in_smem && base <= 32 && hs.n + base <= HC) {
-        long long h = hs.n;
-        if (lane == 0) h = fold_linear<V>(SB, base, Hs, h);
-        hs.n = __shfl_sync(0xffffffffu, h, 0);
+      const int cnt = __popc(svm);
+      int incl = cnt;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int o = __shfl_up_sync(FULL, incl, d);
+        if (lane >= d) incl += o;
+      }
+      const int total = __shfl_sync(FULL, incl, 31);
+      if (pend + total > PC) flush();
+      V* dst = PBf + pend;
+      if (total > PC) {
+        // many survivors: compact them into the block's own slot (every lane
+        // holds its run in registers) and merge them as one batch
+        __syncwarp();
+        dst = reinterpret_cast<V*>(wb + LY::RING + (size_t)s_cur * BB);
+      }
+      int pos = incl - cnt;
+#pragma unroll
+      for (int i = 0; i < NP; ++i)
+        if ((svm >> i) & 1u) dst[pos++] = pt_of(c[i / PPL], i % PPL);
+      if (total > PC) {
+        __syncwarp();
+        hs = merge_block_tree<S, HC>(dst, total, mns, mnc, Hs, gout + ubase, hs);
+        __syncwarp();
       } else {
-        hs = merge_block_tree<S, HC>(SB, base, mns, mnc, Hs, gout + ubase, hs);
+        pend += total;
       }
-      __syncwarp();
     }
     runmax = fmax(runmax, wcur);
     // slide the window: the block after this one becomes current
+    lmc = lmw[0];
     wcur = win[0];
 #pragma unroll
-    for (int i = 0; i + 1 < D; ++i) win[i] = win[i + 1];
+    for (int i = 0; i + 1 < D; ++i) {
+      lmw[i] = lmw[i + 1];
+      win[i] = win[i + 1];
+    }
     s_cur = (s_cur + 1 == R) ? 0 : s_cur + 1;
     s_far = (s_far + 1 == R) ? 0 : s_far + 1;
     s_new = (s_new + 1 == R) ? 0 : s_new + 1;
 
     if (nrem == 0) {
       // unit done: its hood to the output slots, its summary for finalize
+      flush();
       if (hs.in_smem)
         for (long long e = lane; e < hs.n; e += 32) gout[ubase + e] = Hs[e];
       if (spi > 1) {
@@ -1012,6 +1157,13 @@ __global__ void __launch_bounds__(128) ring_hull_kernel(const SlabParams<S> p) {
     advance(cc);
   }
   cp_async_wait<0>();
+  if (p.trace && lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(p.trace) + 1, gtimer());
+  if (p.trace && lane == 0) {
+    p.trace[1024 + 4 * gw + 1] = (long long)gtimer();
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    p.trace[1024 + 4 * gw + 2] = smid;
+  }
 }
 
 // ------------------------------------------------------------ instance kernel
@@ -1493,35 +1645,40 @@ __global__ void pad_fill_kernel(typename PointT<S>::V* padded, const typename Po
 
 // ------------------------------------------------------------------ host side
 
-// Ring kernel lookahead depth D (blocks of 2 KB per warp); selected once per
-// process (HOOD_RING_D=<D> overrides it for experiments).
-static int ring_depth() {
+// Ring kernel shape (D blocks of lookahead, P blocks in flight per warp);
+// selected once per process (HOOD_RING=<D><P>, e.g. 23, overrides it for
+// experiments).
+#define HOOD_RING_SHAPES(X) X(1, 4) X(2, 3) X(2, 4) X(3, 3) X(4, 1) X(2, 6)
+static int ring_shape() {
   static int d = [] {
-    int v = 4;
-    if (const char* e = std::getenv("HOOD_RING_D")) v = std::atoi(e);
-    return (v == 4 || v == 6 || v == 8 || v == 12) ? v : 4;
+    int v = 23;
+    if (const char* e = std::getenv("HOOD_RING")) v = std::atoi(e);
+#define HOOD_RING_OK(D, P) if (v == D * 10 + P) return v;
+    HOOD_RING_SHAPES(HOOD_RING_OK)
+#undef HOOD_RING_OK
+    return 23;
   }();
   return d;
 }
 
-template <class S, int D>
+template <class S, int D, int P>
 static size_t ring_smem() {
-  return (size_t)4 * RingLayout<S, D>::BYTES;
+  return (size_t)4 * RingLayout<S, D, P>::BYTES + 128;  // + alignment pad
 }
 
-template <class S, int D>
+template <class S, int D, int P>
 static int ring_occ_of() {
-  const size_t smem = ring_smem<S, D>();
-  cudaFuncSetAttribute(ring_hull_kernel<S, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem = ring_smem<S, D, P>();
+  cudaFuncSetAttribute(ring_hull_kernel<S, D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int o = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ring_hull_kernel<S, D>, 128, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ring_hull_kernel<S, D, P>, 128, smem);
   return o > 0 ? o : 1;
 }
 
 template <class S>
 int slab_tile_rows(bool hmode) {
   // hmode: points per 2 KB block, in 128-byte chunk rows of K points
-  return hmode ? (RingLayout<S, 6>::BP / PointT<S>::K) : kThreads;
+  return hmode ? (RingLayout<S, 2, 3>::BP / PointT<S>::K) : kThreads;
 }
 
 template <class S>
@@ -1533,11 +1690,11 @@ template <class S>
 int slab_kernel_occupancy() {
   static int occ = -1;
   if (occ < 0) {
-    switch (ring_depth()) {
-      case 4: occ = ring_occ_of<S, 4>(); break;
-      case 8: occ = ring_occ_of<S, 8>(); break;
-      case 12: occ = ring_occ_of<S, 12>(); break;
-      default: occ = ring_occ_of<S, 6>(); break;
+    switch (ring_shape()) {
+#define HOOD_RING_OCC(D, P) \
+  case D * 10 + P: occ = ring_occ_of<S, D, P>(); break;
+      HOOD_RING_SHAPES(HOOD_RING_OCC)
+#undef HOOD_RING_OCC
     }
   }
   return occ;
@@ -1564,11 +1721,11 @@ void launch_slab_kernel(const SlabParams<S>& p, const CUtensorMap* tmap, int gri
     return;
   }
   slab_kernel_occupancy<S>();
-  switch (ring_depth()) {
-    case 4: ring_hull_kernel<S, 4><<<grid, 128, ring_smem<S, 4>(), st>>>(p); break;
-    case 8: ring_hull_kernel<S, 8><<<grid, 128, ring_smem<S, 8>(), st>>>(p); break;
-    case 12: ring_hull_kernel<S, 12><<<grid, 128, ring_smem<S, 12>(), st>>>(p); break;
-    default: ring_hull_kernel<S, 6><<<grid, 128, ring_smem<S, 6>(), st>>>(p); break;
+  switch (ring_shape()) {
+#define HOOD_RING_LAUNCH(D, P) \
+  case D * 10 + P: ring_hull_kernel<S, D, P><<<grid, 128, ring_smem<S, D, P>(), st>>>(p); break;
+    HOOD_RING_SHAPES(HOOD_RING_LAUNCH)
+#undef HOOD_RING_LAUNCH
   }
 }
 
