@@ -302,3 +302,42 @@ def test_graph_capture_replay(oracle_mod):
     h = oracle_mod.upper_hull(p)
     assert int(counts[0]) == len(h)
     assert same(corners[: len(h)].cpu().numpy(), h)
+
+
+def test_cpp_dropin_binary():
+    """tests/cpp/test_dropin.cpp: include/hood_b200.hpp from C++, the
+    reference's Point2 layout, known answers + random sets + errors."""
+    import os
+    import subprocess
+    from paper_1203_5004_b200 import build as Bd
+    Bd.build()
+    exe = os.path.join(os.path.dirname(Bd.SO), "test_dropin")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "OK" in r.stdout
+
+
+def test_sharded_build_on_device(oracle_mod):
+    """distributed.sharded_build with the CUDA build and merge, one rank over
+    NCCL (the N>1 protocol is covered by tests/test_distributed.py on gloo)."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_1203_5004_b200 import distributed as Dz
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        p = W.grid_uniform(1 << 18, seed=31)
+        res = Dz.sharded_build(torch.as_tensor(p).cuda(), x_offset=0.0)
+        assert res.exchanges == 1
+        assert same(res.hull.cpu().numpy(), oracle_mod.upper_hull(p))
+        res = Dz.sharded_build(torch.as_tensor(W.arc(1 << 14)).cuda(), cap=256)
+        assert res.exchanges == 2
+        assert same(res.hull.cpu().numpy(), oracle_mod.upper_hull(W.arc(1 << 14)))
+    finally:
+        dist.destroy_process_group()
