@@ -397,7 +397,9 @@ def run_ours(args):
             t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t[0])
-        d2h = inst * 4 + int(cnt_h.sum()) * bpp
+        # counts + corners as hood_build_host copies them (batched: one
+        # strided copy of the widest instance's count per instance)
+        d2h = inst * 4 + (int(cnt_h.max()) * inst if inst > 1 else int(cnt_h[0])) * bpp
         e2e = {"value": world * n / (e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e_ms,
                "h2d_bytes_per_step": n * bpp, "d2h_bytes_per_step": d2h}
 

@@ -375,9 +375,15 @@ int build_host(hood_ctx* ctx, const S* h_pts, long long n, long long block_len, 
   if (pl.instances == 1) {
     cudaMemcpy(h_corners, d_out, (size_t)h_counts[0] * sizeof(V), cudaMemcpyDeviceToHost);
   } else {
-    for (long long i = 0; i < pl.instances; ++i)
-      cudaMemcpyAsync(h_corners + 2 * i * pl.L, d_out + 2 * i * pl.L, (size_t)h_counts[i] * sizeof(V),
-                      cudaMemcpyDeviceToHost, sk);
+    // every instance's corners in one strided copy: rows of L slots, the
+    // widest instance's count of columns
+    int widest = 0;
+    for (long long i = 0; i < pl.instances; ++i) widest = std::max(widest, h_counts[i]);
+    if (widest > 0) {
+      const size_t pitch = (size_t)pl.L * sizeof(V);
+      cudaMemcpy2DAsync(h_corners, pitch, d_out, pitch, (size_t)widest * sizeof(V), (size_t)pl.instances,
+                        cudaMemcpyDeviceToHost, sk);
+    }
     cudaStreamSynchronize(sk);
   }
   return cudaGetLastError() == cudaSuccess ? HOOD_OK : HOOD_ERR_CUDA;

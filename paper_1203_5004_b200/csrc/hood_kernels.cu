@@ -44,7 +44,6 @@ namespace hood_b200 {
 
 template <class S> struct HCap { static constexpr int value = 128; };  // running hood kept in smem (corners)
 
-constexpr int kSeqMax = 96;                   // survivors per tile folded point by point
 
 __device__ __forceinline__ unsigned char* align1024(unsigned char* p) {
   const unsigned a = smem_u32(p);
