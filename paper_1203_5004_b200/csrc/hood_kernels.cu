@@ -4,35 +4,24 @@
 // over REMOTE-padded blocks, each round touching all 36n bytes of hood /
 // newhood / scratch (psim.cpp:40-47).  Here one HBM pass does the work.
 //
-// slab_hull_kernel (instances spanning >= 1 tile; the hot kernel, HBM-bound:
-//   it reads the 8n / 16n input bytes exactly once).  Persistent CTAs, 2 per
-//   SM, each owning a contiguous x-slab streamed in 32 KB tiles through a
-//   3-stage TMA ring (cp.async.bulk.tensor, 128B swizzle, mbarrier
-//   complete_tx).  Warp-specialised:
-//     * 8 compute warps, one 128-byte chunk row (16 float2 / 8 double2
-//       points) per thread.  Per tile: max y of its chunk of the NEXT tile
-//       (one tile of lookahead), one named barrier to exchange warp maxima,
-//       then every warp gets an anchor height
-//         tau = min(max y left of the warp in the slab, max y right of it
-//                   up to the end of the next tile).
-//       A point with y < tau lies strictly below the chord between two input
-//       points that straddle it, so it cannot be a corner of the final hood;
-//       one compare drops it.  The rare survivors run the reference monotone
-//       chain (oracle.cpp:7-20) in the thread's own swizzled smem row.  x is
-//       checked strictly increasing on the way (validate_points,
-//       hoodbuf.cpp:48-58).
-//     * 1 merger warp: consumes each tile's chunk hoods (mbarrier `ready`),
-//       folds them into the slab's running hood -- point-by-point chain
-//       pushes when few survive (the common case), a warp merge tree + one
-//       bridge (the reference's g/f classifiers as monotone searches,
-//       kernel.hpp:31-67, splice kernel.cpp:117-137) when many do -- then
-//       releases the stage and issues the next TMA load.
-// instance_hull_kernel (batched instances shorter than a tile): whole
-//   instances per tile, exact per-chunk anchors inside every instance, CTA
-//   merge tree per instance, hood written straight to the output slots.
-// finalize_kernel: one CTA per instance spanning several slabs: cull slab
-//   hoods against the slab maxima on both sides, then hull the survivors
-//   (chain in smem, or a merge tree in place in HBM for huge hoods).
+// ring_hull_kernel (instances of >= one 2 KB block; the hot kernel, HBM-bound:
+//   it reads the 8n / 16n input bytes exactly once).  Every warp streams its
+//   own sequence of contiguous x-units through a per-warp cp.async smem ring,
+//   drops every point lying below the chord of two input points that straddle
+//   it with one compare per lane run (y anchors from the blocks on both sides),
+//   checks x strictly increasing (validate_points, hoodbuf.cpp:48-58), and
+//   folds the rare survivors into the unit's hood with the reference monotone
+//   chain (oracle.cpp:7-20) or a warp merge tree + bridge search (the g/f
+//   classifiers of kernel.hpp:31-67 as monotone searches, splice
+//   kernel.cpp:117-137).  See the comment at the kernel.
+// instance_hull_kernel (batched instances shorter than a block): whole
+//   instances per TMA tile (cp.async.bulk.tensor, 128B swizzle, mbarrier
+//   ring), exact per-chunk anchors inside every instance, CTA merge tree per
+//   instance, hood written straight to the output slots.
+// finalize_kernel: one CTA per instance spanning several units: cull unit
+//   hoods against the units' anchor points on both sides, then hull the
+//   survivors (monotone chain in smem, or a merge tree in place in HBM for
+//   huge hoods).
 // pad_fill_kernel: optional REMOTE-padded n-slot output (HoodBuffer layout).
 #include "hood_device.cuh"
 #include "hood_kernels.cuh"
@@ -1398,11 +1387,9 @@ constexpr int kFinCandCap = 32;    // corners staged per candidate
 //   2. One warp per remaining slab reads its corners coalesced and stages the
 //      run strictly above A-C (one contiguous run: a concave chain meets a
 //      line once) in smem; the runs are then compacted in x order.
-//   3. The survivors are pruned in parallel rounds: a point not strictly
-//      above the chord of its current neighbours is not a hull corner and is
-//      dropped (geom.hpp:22-28 predicate, canonical order); when a round drops
-//      nothing the chain is strictly concave, i.e. the strict upper hull --
-//      exactly what oracle.cpp:7-20 returns.
+//   3. The compacted survivors (x order) go through one monotone chain
+//      (oracle.cpp:7-20, geom.hpp:22-28 predicate in canonical order): the
+//      strict upper hull.
 // Huge survivor sets (the arc) merge the slab hoods in place in HBM instead.
 template <class S>
 __global__ void __launch_bounds__(kFinThreads, 1) finalize_kernel(const FinalizeParams<S> p) {
