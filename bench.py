@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--log2n", type=int, default=None, help="override n for configs 2/4")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-kernel-events", action="store_true",
+                    help="capture the step graph without the event pair around the slab kernel (roofline unmeasured)")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
 
@@ -321,47 +323,68 @@ def run_ours(args):
 
     # One build = one CUDA graph replay on a single GPU (the C-ABI builds are
     # capture-safe): the timed region then holds the kernels and nothing of the
-    # Python / ctypes launch path.  The slab kernel is bracketed by a captured
-    # event pair for the roofline.  Multi-GPU steps (NCCL exchange) run eagerly.
-    graph = None
+    # Python / ctypes launch path.  The timed steps run a plain graph; the
+    # roofline comes from a second pass over a graph whose slab kernel is
+    # bracketed by a captured event pair (events inside the graph cost a few
+    # microseconds of step time, so they stay out of the timed steps).
+    # Multi-GPU steps (NCCL exchange) run eagerly.
+    graph = prof_graph = None
     if world == 1:
-        ctx.set_profile_events(kb, ka)
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             one_step()
-        ctx.set_profile_events(None, None)
         launches_per_step = ctx.last_launch_count()
         step = graph.replay
+        if not args.no_kernel_events:
+            ctx.set_profile_events(kb, ka)
+            prof_graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(prof_graph):
+                one_step()
+            ctx.set_profile_events(None, None)
     else:
         launches_per_step = None
         step = one_step
     for _ in range(args.warmup):
         flush_l2()
         step()
+        if prof_graph is not None:
+            flush_l2()
+            prof_graph.replay()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     launches = 0
-    kern_ms = []
     sampler = ClockSampler(local)
     with sampler:
         for i in range(args.steps):
             flush_l2()
-            if graph is None:
-                ctx.set_profile_events(kb, ka)
             ev0[i].record(stream)
             step()
             ev1[i].record(stream)
-            if graph is None:
-                ctx.set_profile_events(None, None)
             launches += (launches_per_step if launches_per_step is not None else ctx.last_launch_count() + 1)
-            ev1[i].synchronize()
-            kern_ms.append(kb.elapsed_time(ka))
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    # roofline pass: the slab kernel alone, event-timed on its own stream
+    kern_ms = []
+    if not args.no_kernel_events:
+        for i in range(args.steps):
+            flush_l2()
+            if prof_graph is not None:
+                prof_graph.replay()
+            else:
+                ctx.set_profile_events(kb, ka)
+                one_step()
+                ctx.set_profile_events(None, None)
+            ka.synchronize()
+            kern_ms.append(kb.elapsed_time(ka))
+    else:
+        kern_ms.append(float("nan"))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
     ms = statistics.mean(step_ms)
     kms = statistics.mean(kern_ms)

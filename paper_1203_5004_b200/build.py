@@ -39,6 +39,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
                "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-o", SO]
         if verbose:
             cmd += ["-Xptxas", "-v"]
+        cmd += os.environ.get("HOOD_NVCC_EXTRA", "").split()  # experiments only (e.g. -DHOOD_RING_COUNTERS)
         cmd += [os.path.join(CSRC, f) for f in SOURCES]
         cmd += ["-lcuda"] if False else []
         subprocess.run(cmd, check=True)

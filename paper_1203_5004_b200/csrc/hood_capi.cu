@@ -204,7 +204,7 @@ FinalizeParams<S> finalize_params(hood_ctx* ctx, const Plan& pl, void* corners, 
   f.seg_stride = 0;
   f.slabs_per_inst = pl.spi;
   f.L = pl.L;
-  f.fcap = 2048;
+  f.fcap = (int)(32768 / sizeof(V));  // 64 KB of survivor stack, as double2
   f.trace = ctx->trace ? ctx->trace + 7 * 64 : nullptr;
   return f;
 }
@@ -253,7 +253,8 @@ int build_device(hood_ctx* ctx, const S* pts, long long n, long long block_len, 
   if (ctx->prof_after) record_event(ctx->prof_after, st);
   int launches = 1;
   if (pl.hmode && pl.spi > 1) {
-    launch_finalize<S>(finalize_params<S>(ctx, pl, corners, counts), (int)pl.instances, st);
+    launch_finalize<S>(finalize_params<S>(ctx, pl, corners, counts), (int)pl.instances, st,
+                       /*pdl=*/!ctx->prof_after);
     debug_check("finalize", st);
     ++launches;
   }
@@ -413,7 +414,7 @@ int merge_segments(hood_ctx* ctx, const S* seg_pts, const int* counts, long long
   f.seg_stride = stride;
   f.slabs_per_inst = (int)G;
   f.L = G * stride;
-  f.fcap = 2048;
+  f.fcap = (int)(32768 / sizeof(V));  // 64 KB of survivor stack, as double2
   launch_finalize<S>(f, 1, st);
   ctx->last_stream = st;
   ctx->have_last = true;

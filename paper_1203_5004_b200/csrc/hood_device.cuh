@@ -70,6 +70,15 @@ __device__ __forceinline__ bool above(const float2& a, const float2& b, const fl
   return above_slow(a.x, a.y, b.x, b.y, c.x, c.y);  // rare: keep it out of the hot code
 }
 
+// The reference predicate evaluated in double for either storage (floats
+// widen exactly): the same answer as above(), without the filter.
+__device__ __forceinline__ bool above_exact(const double2& a, const double2& b, const double2& c) {
+  return above_d(a.x, a.y, b.x, b.y, c.x, c.y);
+}
+__device__ __forceinline__ bool above_exact(const float2& a, const float2& b, const float2& c) {
+  return above_d((double)a.x, (double)a.y, (double)b.x, (double)b.y, (double)c.x, (double)c.y);
+}
+
 // Three-way version (+1 above, -1 below, 0 on the chord) with the same
 // semantics: the sign of the reference's double orient(b, a, c).
 __device__ __forceinline__ int orient_sign_d(double ax, double ay, double bx, double by, double cx, double cy) {

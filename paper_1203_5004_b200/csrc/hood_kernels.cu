@@ -588,11 +588,11 @@ __device__ __forceinline__ void cp_async_wait() {
 // Per-warp shared memory of the ring kernel: R = D + P + 1 block slots (the
 // block being processed, D landed blocks of lookahead, P blocks in flight),
 // the unit's running hood and a small buffer of pending survivors.
-template <class S, int D, int P>
+template <class S, int D, int P, int U_>
 struct RingLayout {
   using V = typename PointT<S>::V;
   static constexpr size_t up(size_t x, size_t a) { return (x + a - 1) / a * a; }
-  static constexpr int U = 4;                                           // 16-byte chunks per lane per block
+  static constexpr int U = U_;                                          // 16-byte chunks per lane per block
   static constexpr int R = D + P + 1;                                   // ring slots
   static constexpr int BP = 32 * U * Ld16<S>::PPL;                      // points per block
   static constexpr size_t BB = 32 * U * 16;                             // bytes per block
@@ -758,11 +758,11 @@ __device__ __forceinline__ int ring_rot(int l) {
 //   tree + bridge, kernel.hpp:31-67, when many).  A block at an instance edge
 //   (no anchor on one side) gets exact per-point anchors from warp max-scans.
 // Every warp touches only its own smem, so no CTA barrier is ever needed.
-template <class S, int D, int P>
+template <class S, int D, int P, int U_>
 __global__ void __maxnreg__(HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams<S> p) {
   using V = typename PointT<S>::V;
   using L = typename Ld16<S>::T;
-  using LY = RingLayout<S, D, P>;
+  using LY = RingLayout<S, D, P, U_>;
   constexpr int U = LY::U, R = LY::R, PPL = Ld16<S>::PPL;
   constexpr int NP = U * PPL;  // points per lane run
   constexpr int BP = LY::BP;
@@ -906,13 +906,51 @@ __global__ void __maxnreg__(HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams
     return fmax(m0, m1);
   };
 
+  // a dependent finalize may be scheduled now; it waits for our completion
+  asm volatile("griddepcontrol.launch_dependents;");
   // profiling (p.trace, globaltimer ns): [0] first warp entry, [1] last warp
   // exit, [2] last prologue end; per warp gw at [1024 + 4 gw]: entry, exit, SM
   if (p.trace && lane == 0) atomicMin(reinterpret_cast<unsigned long long*>(p.trace), gtimer());
   if (p.trace && lane == 0) p.trace[1024 + 4 * gw] = (long long)gtimer();
+#ifdef HOOD_RING_COUNTERS
+  int n_cand = 0, n_edge = 0, n_many = 0;
+  long long c_cand = 0, c_flush = 0, c_land = 0;
+#define HOOD_COUNT(x) ++x
+#define HOOD_TIC() const long long tic_ = clock64()
+#define HOOD_TOC(acc) acc += clock64() - tic_
+#else
+#define HOOD_COUNT(x)
+#define HOOD_TIC()
+#define HOOD_TOC(acc)
+#endif
   UnitCur cc{0, 0, 0};
   seek(cc);
   if (!(cc.b < cc.e)) return;
+
+  // lane partial maxima of the edge anchors of the unit [b, e): up to EXT
+  // input points on each side of it inside its instance
+  auto ext_partial = [&](int b, int e, S& pl, S& pr) {
+    const long long ibase = (long long)(b / bpi) * p.L;
+    const long long lim = min(n, ibase + p.L);
+    const long long ub = (long long)b * BP, ue = min((long long)e * BP, lim);
+    const long long l0 = max(ibase, ub - EXT), r1 = min(min(lim, p.read_lim), ue + EXT);
+    pl = NEG;
+    pr = NEG;
+    if (ub > ibase) {
+#pragma unroll
+      for (int t = 0; t < EXT / 32; ++t) {  // independent loads: one latency
+        const long long i = ub - EXT + t * 32 + lane;
+        if (i >= l0) pl = fmax(pl, gpts[i].y);
+      }
+    }
+    if (ue < r1) {
+#pragma unroll
+      for (int t = 0; t < EXT / 32; ++t) {
+        const long long j = ue + t * 32 + lane;
+        if (j < r1) pr = fmax(pr, gpts[j].y);
+      }
+    }
+  };
 
   // prologue: sequence blocks 0 .. D+P-1 in flight (one commit group each),
   // then blocks 0 .. D-1 landed
@@ -923,6 +961,11 @@ __global__ void __maxnreg__(HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams
     cp_async_commit();
     advance(ci);
   }
+  // the first unit's anchors and predecessor x: loaded behind the prologue
+  // copies, consumed after they land
+  S pre_l, pre_r;
+  ext_partial(cc.b, cc.e, pre_l, pre_r);
+  const S pre_x = (cc.b % bpi) != 0 ? gpts[(long long)cc.b * BP - 1].x : NEG;
   cp_async_wait<P>();
   __syncwarp();
   UnitCur cf = cc;
@@ -945,7 +988,12 @@ __global__ void __maxnreg__(HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams
     }
     cf_first = advance(cf);
   };
-  land_next(0, lmc, wcur);
+  {  // the first block: its predecessor x was loaded up front
+    xcf = pre_x;
+    lmc = land(cf.b, 0, (cf.b % bpi) != 0, xcf);
+    wcur = warp_max_fast(lmc);
+    cf_first = advance(cf);
+  }
 #pragma unroll
   for (int i = 0; i + 1 < D; ++i) land_next(i + 1, lmw[i], win[i]);
   lmw[D - 1] = NEG;
@@ -968,7 +1016,8 @@ __global__ void __maxnreg__(HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams
   auto flush = [&]() {
     __syncwarp();
     if (pend == 0) return;
-    if (hs.in_smem && pend <= 32 && hs.n + pend <= HC) {
+    HOOD_TIC();
+    if (hs.in_smem && hs.n + pend <= HC) {  // pend <= PC: one lane pushes them
       long long h = hs.n;
       if (lane == 0) h = fold_linear<V>(PBf, pend, Hs, h);
       hs.n = __shfl_sync(FULL, h, 0);
@@ -977,6 +1026,7 @@ __global__ void __maxnreg__(HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams
     }
     pend = 0;
     __syncwarp();
+    HOOD_TOC(c_flush);
   };
 
 #pragma unroll 1
@@ -987,29 +1037,21 @@ __global__ void __maxnreg__(HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams
     advance(ci);
     cp_async_wait<P>();
     __syncwarp();  // the landed block was copied by all lanes
-    land_next(s_far, lmw[D - 1], win[D - 1]);
+    {
+      HOOD_TIC();
+      land_next(s_far, lmw[D - 1], win[D - 1]);
+      HOOD_TOC(c_land);
+    }
 
     if (fresh) {
       fresh = false;
       u = p.unit_lo + gw + (long long)cc.r * nwarps;
       inst = spi == 1 ? (int)u : (int)u / spi;
-      const long long ibase = (long long)inst * p.L;
-      const long long lim = min(n, ibase + p.L);
       ubase = (long long)cc.b * BP;
-      const long long uend = min((long long)cc.e * BP, lim);
       // edge anchors: max y of up to EXT points on each side of the unit
-      ext_l = NEG;
-      ext_r = NEG;
-      if (ubase > ibase) {
-        const long long l0 = max(ibase, ubase - EXT);
-        for (long long i = l0 + lane; i < ubase; i += 32) ext_l = fmax(ext_l, gpts[i].y);
-        ext_l = warp_max(ext_l);
-      }
-      if (uend < lim) {
-        const long long r1 = min(min(lim, p.read_lim), uend + EXT);
-        for (long long i = uend + lane; i < r1; i += 32) ext_r = fmax(ext_r, gpts[i].y);
-        ext_r = warp_max(ext_r);
-      }
+      if (cc.r != 0) ext_partial(cc.b, cc.e, pre_l, pre_r);
+      ext_l = __any_sync(FULL, pre_l != NEG) ? warp_max(pre_l) : NEG;
+      ext_r = __any_sync(FULL, pre_r != NEG) ? warp_max(pre_r) : NEG;
       runmax = ext_l;
       hs = HoodState{0, 1};
       pend = 0;
@@ -1026,6 +1068,8 @@ __global__ void __maxnreg__(HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams
 
     // lane runs reaching tau (every run at an instance edge)
     const unsigned cm = tau != NEG ? __ballot_sync(FULL, !(lmc < tau)) : FULL;
+    if (cm != 0) HOOD_COUNT(n_cand);
+    HOOD_TIC();
     if (cm != 0 && cm != FULL && __popc(cm) <= 2) {
       // a few runs: re-read them point-per-lane, queue the survivors
       unsigned cr = cm;
@@ -1048,6 +1092,8 @@ __global__ void __maxnreg__(HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams
     } else if (cm != 0) {
       // many runs (arc-like input) or an instance edge (exact per-point
       // anchors on the side(s) without a block anchor): the whole block
+      if (tau == NEG) HOOD_COUNT(n_edge);
+      else HOOD_COUNT(n_many);
       unsigned svm;
       L c[U];
       {
@@ -1091,6 +1137,7 @@ __global__ void __maxnreg__(HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams
         pend += total;
       }
     }
+    HOOD_TOC(c_cand);
     runmax = fmax(runmax, wcur);
     // slide the window: the block after this one becomes current
     lmc = lmw[0];
@@ -1151,6 +1198,12 @@ __global__ void __maxnreg__(HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams
     unsigned smid;
     asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
     p.trace[1024 + 4 * gw + 2] = smid;
+#ifdef HOOD_RING_COUNTERS
+    p.trace[1024 + 4 * gw + 3] = ((long long)n_cand << 32) | (n_edge << 16) | n_many;
+    p.trace[1024 + 4 * 8192 + 4 * gw] = c_cand;
+    p.trace[1024 + 4 * 8192 + 4 * gw + 1] = c_flush;
+    p.trace[1024 + 4 * 8192 + 4 * gw + 2] = c_land;
+#endif
   }
 }
 
@@ -1406,18 +1459,31 @@ __global__ void __launch_bounds__(kFinThreads, 1) finalize_kernel(const Finalize
   const V NOPT = V{NEG, NEG};
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  long long* nsd = reinterpret_cast<long long*>(smem_raw);  // [M] tree path
-  int* ncd = reinterpret_cast<int*>(nsd + M);               // [M]
-  V* shV = reinterpret_cast<V*>((reinterpret_cast<uintptr_t>(ncd + M) + 15) & ~(uintptr_t)15);  // [NWP]
-  int* shI = reinterpret_cast<int*>(shV + NWP);             // [NWP + 8]
-  long long* cb = reinterpret_cast<long long*>((reinterpret_cast<uintptr_t>(shI + NWP + 8) + 7) & ~(uintptr_t)7);  // [MAXC]
-  int* cc = reinterpret_cast<int*>(cb + MAXC);              // [MAXC] corner count
-  int* cn = cc + MAXC;                                      // [MAXC] alive count
-  V* cA = reinterpret_cast<V*>((reinterpret_cast<uintptr_t>(cn + MAXC) + 15) & ~(uintptr_t)15);  // [MAXC]
-  V* cC = cA + MAXC;                                        // [MAXC]
-  V* stg = cC + MAXC;                                       // [MAXC][CAP] staged alive runs
-  V* F = stg + MAXC * CAP;                                  // [2][fcap] ping-pong survivors
+  // carve-up by byte offsets from smem_raw (pointer arithmetic on the
+  // shared array keeps every access LDS/STS; uintptr_t rounding would not)
+  auto up16 = [](size_t x) { return (x + 15) & ~(size_t)15; };
+  const size_t o_ncd = (size_t)M * sizeof(long long);
+  const size_t o_shV = up16(o_ncd + (size_t)M * sizeof(int));
+  const size_t o_shI = o_shV + NWP * sizeof(V);
+  const size_t o_cb = up16(o_shI + (NWP + 8) * sizeof(int));
+  const size_t o_cc = o_cb + MAXC * sizeof(long long);
+  const size_t o_cn = o_cc + MAXC * sizeof(int);
+  const size_t o_cA = up16(o_cn + MAXC * sizeof(int));
+  long long* nsd = reinterpret_cast<long long*>(smem_raw);          // [M] tree path
+  int* ncd = reinterpret_cast<int*>(smem_raw + o_ncd);              // [M]
+  V* shV = reinterpret_cast<V*>(smem_raw + o_shV);                  // [NWP]
+  int* shI = reinterpret_cast<int*>(smem_raw + o_shI);              // [NWP + 8]
+  long long* cb = reinterpret_cast<long long*>(smem_raw + o_cb);    // [MAXC]
+  int* cc = reinterpret_cast<int*>(smem_raw + o_cc);                // [MAXC] corner count
+  int* cn = reinterpret_cast<int*>(smem_raw + o_cn);                // [MAXC] alive count
+  const size_t o_stg = o_cA + 2 * MAXC * sizeof(double2);
+  V* cA = reinterpret_cast<V*>(smem_raw + o_cA);                    // [MAXC]
+  V* cC = cA + MAXC;                                                // [MAXC]
+  // staged alive runs, widened to double (exact) for the final chain
+  double2* stg = reinterpret_cast<double2*>(smem_raw + o_stg);      // [MAXC][CAP]
+  V* F = reinterpret_cast<V*>(smem_raw + o_stg + (size_t)MAXC * CAP * sizeof(double2));  // [2][fcap]
 
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the slab kernel has completed
   if (p.trace && tid == 0) p.trace[0] = clock64();
   const int per = (M + kFinThreads - 1) / kFinThreads;
   long long sb[R];
@@ -1481,72 +1547,83 @@ __global__ void __launch_bounds__(kFinThreads, 1) finalize_kernel(const Finalize
         ++cpos;
       }
     __syncthreads();
-    // one warp per candidate: stage its corners strictly above the chord A-C
-    for (int c = warp; c < C; c += NWP) {
-      const long long b = cb[c];
-      const int cnt = cc[c];
-      const V A = cA[c], Cp = cC[c];
-      const bool both = A.y > NEG && Cp.y > NEG;  // without both anchors nothing is culled
-      int n_alive = 0;
-      for (int e0 = 0; e0 < cnt; e0 += 32) {
-        const int e = e0 + lane;
-        V v = NOPT;
-        bool keep = false;
-        if (e < cnt) {
-          v = gout[b + e];
-          keep = !both || above(A, v, Cp);
-        }
-        const unsigned mk = __ballot_sync(0xffffffffu, keep);
-        const int pos = n_alive + __popc(mk & ((1u << lane) - 1u));
-        if (keep && pos < CAP) stg[c * CAP + pos] = v;
-        n_alive += __popc(mk);
+    // one warp per candidate: stage its corners strictly above the chord A-C;
+    // the first 32 corners of four candidates per warp are loaded at once
+    constexpr int GB = 4;
+    for (int c0 = warp; c0 < C; c0 += GB * NWP) {
+      V v[GB];
+#pragma unroll
+      for (int g = 0; g < GB; ++g) {
+        const int c = c0 + g * NWP;
+        v[g] = (c < C && lane < cc[c]) ? gout[cb[c] + lane] : NOPT;
       }
-      if (lane == 0) cn[c] = n_alive;
+#pragma unroll
+      for (int g = 0; g < GB; ++g) {
+        const int c = c0 + g * NWP;
+        if (c >= C) break;
+        const int cnt = cc[c];
+        const V A = cA[c], Cp = cC[c];
+        const bool both = A.y > NEG && Cp.y > NEG;  // without both anchors nothing is culled
+        int n_alive = 0;
+        for (int e0 = 0; e0 < cnt; e0 += 32) {
+          const int e = e0 + lane;
+          V w = e0 == 0 ? v[g] : NOPT;
+          bool keep = false;
+          if (e < cnt) {
+            if (e0 != 0) w = gout[cb[c] + e];
+            keep = !both || above(A, w, Cp);
+          }
+          const unsigned mk = __ballot_sync(0xffffffffu, keep);
+          const int pos = n_alive + __popc(mk & ((1u << lane) - 1u));
+          if (keep && pos < CAP) stg[c * CAP + pos] = make_double2((double)w.x, (double)w.y);
+          n_alive += __popc(mk);
+        }
+        if (lane == 0) cn[c] = n_alive;
+      }
     }
     __syncthreads();
     if (p.trace && tid == 0) p.trace[3] = clock64();
-    int ovf = 0, A = 0;
+    int ovf = 0;
     for (int c = tid; c < C; c += kFinThreads) ovf |= cn[c] > CAP;
     ovf = __syncthreads_or(ovf);
-    const int v0 = tid < C ? min(cn[tid], CAP) : 0;
-    const int o0 = block_excl_sum<NWP>(v0, shI, &A);
-    if (!ovf && A <= p.fcap) {
-      V* Fa = F;
-        // compact the staged runs in x order; each run is a strict hood
-      long long* rns = nsd;  // reuse the tree-node arrays: run start / size
+    if (!ovf) {
+      long long* rns = nsd;  // reuse the tree-node arrays: hull start / size
       int* rnc = ncd;
-      if (tid < C) {
-        for (int e = 0; e < cn[tid]; ++e) Fa[o0 + e] = stg[tid * CAP + e];
-        rns[tid] = o0;
-        rnc[tid] = cn[tid];
-      }
-      __syncthreads();
       if (p.trace && tid == 0) p.trace[4] = clock64();
-      // one monotone chain (oracle.cpp:7-20) over the few survivors, in
-      // place (the stack never passes the point being read)
+      // one monotone chain (oracle.cpp:7-20) straight over the staged runs
+      // (candidate order = x order) in double (the reference predicate
+      // itself; float inputs were widened exactly), stack in smem
+      double2* Hd = reinterpret_cast<double2*>(F);
+      int A = 0;
       if (tid == 0) {
+        if (p.trace) p.trace[10] = clock64();
         int h = 0;
-        V h1 = V{}, h2 = V{};
-        for (int i = 0; i < A; ++i) {
-          const V q = Fa[i];
-          while (h >= 2 && !above(h2, h1, q)) {
-            --h;
-            h1 = h2;
-            if (h >= 2) h2 = Fa[h - 2];
+        double2 h1 = make_double2(0, 0), h2 = h1;
+        for (int c = 0; c < C; ++c) {
+          const int m = cn[c];
+          const double2* run = stg + c * CAP;
+          for (int e = 0; e < m; ++e) {
+            const double2 q = run[e];
+            while (h >= 2 && !above(h2, h1, q)) {
+              --h;
+              h1 = h2;
+              if (h >= 2) h2 = Hd[h - 2];
+            }
+            Hd[h] = q;
+            ++h;
+            h2 = h1;
+            h1 = q;
           }
-          Fa[h] = q;
-          ++h;
-          h2 = h1;
-          h1 = q;
+          A += m;
         }
         rns[0] = 0;
         rnc[0] = h;
+        if (p.trace) p.trace[11] = clock64();
       }
       __syncthreads();
       if (p.trace && tid == 0) p.trace[5] = clock64();
-      const long long rs = rns[0];
       const int n = rnc[0];
-      for (int e = tid; e < n; e += kFinThreads) gout[ibase + e] = Fa[rs + e];
+      for (int e = tid; e < n; e += kFinThreads) gout[ibase + e] = make_vec<V>((S)Hd[e].x, (S)Hd[e].y);
       if (tid == 0) p.out_counts[blockIdx.x] = n;
       if (p.trace && tid == 0) {
         p.trace[6] = clock64();
@@ -1631,40 +1708,45 @@ __global__ void pad_fill_kernel(typename PointT<S>::V* padded, const typename Po
 
 // ------------------------------------------------------------------ host side
 
-// Ring kernel shape (D blocks of lookahead, P blocks in flight per warp);
-// selected once per process (HOOD_RING=<D><P>, e.g. 23, overrides it for
-// experiments).
-#define HOOD_RING_SHAPES(X) X(1, 4) X(2, 3) X(2, 4) X(3, 3) X(4, 1) X(2, 6)
+// Ring kernel shape: D blocks of lookahead, P blocks in flight per warp, U
+// 16-byte chunks per lane per block (blocks of 2 KB for U = 4, 4 KB for
+// U = 8); selected once per process (HOOD_RING=<D><P><U>, e.g. 234, overrides
+// it for experiments).
+#define HOOD_RING_SHAPES(X) X(2, 3, 4) X(1, 2, 4) X(2, 2, 4) X(1, 2, 8) X(1, 3, 8) X(2, 2, 8)
+// measured best (B200, round 1): float2 (1, 2, 8), double2 (2, 2, 8)
+template <class S>
+constexpr int kRingDefault = sizeof(S) == 4 ? 128 : 228;
+template <class S>
 static int ring_shape() {
   static int d = [] {
-    int v = 23;
+    int v = kRingDefault<S>;
     if (const char* e = std::getenv("HOOD_RING")) v = std::atoi(e);
-#define HOOD_RING_OK(D, P) if (v == D * 10 + P) return v;
+#define HOOD_RING_OK(D, P, U) if (v == D * 100 + P * 10 + U) return v;
     HOOD_RING_SHAPES(HOOD_RING_OK)
 #undef HOOD_RING_OK
-    return 23;
+    return kRingDefault<S>;
   }();
   return d;
 }
 
-template <class S, int D, int P>
+template <class S, int D, int P, int U>
 static size_t ring_smem() {
-  return (size_t)4 * RingLayout<S, D, P>::BYTES + 128;  // + alignment pad
+  return (size_t)4 * RingLayout<S, D, P, U>::BYTES + 128;  // + alignment pad
 }
 
-template <class S, int D, int P>
+template <class S, int D, int P, int U>
 static int ring_occ_of() {
-  const size_t smem = ring_smem<S, D, P>();
-  cudaFuncSetAttribute(ring_hull_kernel<S, D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem = ring_smem<S, D, P, U>();
+  cudaFuncSetAttribute(ring_hull_kernel<S, D, P, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int o = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ring_hull_kernel<S, D, P>, 128, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ring_hull_kernel<S, D, P, U>, 128, smem);
   return o > 0 ? o : 1;
 }
 
 template <class S>
 int slab_tile_rows(bool hmode) {
-  // hmode: points per 2 KB block, in 128-byte chunk rows of K points
-  return hmode ? (RingLayout<S, 2, 3>::BP / PointT<S>::K) : kThreads;
+  // hmode: points per ring block, in 128-byte chunk rows of K points
+  return hmode ? 32 * (ring_shape<S>() % 10) * Ld16<S>::PPL / PointT<S>::K : kThreads;
 }
 
 template <class S>
@@ -1676,9 +1758,9 @@ template <class S>
 int slab_kernel_occupancy() {
   static int occ = -1;
   if (occ < 0) {
-    switch (ring_shape()) {
-#define HOOD_RING_OCC(D, P) \
-  case D * 10 + P: occ = ring_occ_of<S, D, P>(); break;
+    switch (ring_shape<S>()) {
+#define HOOD_RING_OCC(D, P, U) \
+  case D * 100 + P * 10 + U: occ = ring_occ_of<S, D, P, U>(); break;
       HOOD_RING_SHAPES(HOOD_RING_OCC)
 #undef HOOD_RING_OCC
     }
@@ -1707,9 +1789,9 @@ void launch_slab_kernel(const SlabParams<S>& p, const CUtensorMap* tmap, int gri
     return;
   }
   slab_kernel_occupancy<S>();
-  switch (ring_shape()) {
-#define HOOD_RING_LAUNCH(D, P) \
-  case D * 10 + P: ring_hull_kernel<S, D, P><<<grid, 128, ring_smem<S, D, P>(), st>>>(p); break;
+  switch (ring_shape<S>()) {
+#define HOOD_RING_LAUNCH(D, P, U) \
+  case D * 100 + P * 10 + U: ring_hull_kernel<S, D, P, U><<<grid, 128, ring_smem<S, D, P, U>(), st>>>(p); break;
     HOOD_RING_SHAPES(HOOD_RING_LAUNCH)
 #undef HOOD_RING_LAUNCH
   }
@@ -1723,7 +1805,7 @@ size_t finalize_smem(int fcap_bytes, int slabs) {
 }
 
 template <class S>
-void launch_finalize(const FinalizeParams<S>& p, int instances, cudaStream_t st) {
+void launch_finalize(const FinalizeParams<S>& p, int instances, cudaStream_t st, bool pdl) {
   using V = typename PointT<S>::V;
   const size_t bytes = finalize_smem(p.fcap * (int)sizeof(V), p.slabs_per_inst);
   static bool attr = false;
@@ -1731,7 +1813,25 @@ void launch_finalize(const FinalizeParams<S>& p, int instances, cudaStream_t st)
     cudaFuncSetAttribute(finalize_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  finalize_kernel<S><<<instances, kFinThreads, bytes, st>>>(p);
+  if (!pdl) {
+    finalize_kernel<S><<<instances, kFinThreads, bytes, st>>>(p);
+    return;
+  }
+  // programmatic dependent launch: finalize is scheduled while the slab
+  // kernel drains (it triggers at its start) and waits in griddepcontrol.wait
+  // for the slab kernel's completion and memory -- the launch gap overlaps
+  // the slab kernel's tail
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)instances);
+  cfg.blockDim = dim3(kFinThreads);
+  cfg.dynamicSmemBytes = bytes;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, finalize_kernel<S>, p);
 }
 
 template <class S>
@@ -1745,8 +1845,8 @@ void launch_pad_fill(void* padded, const void* corners, const int* counts, long 
 
 template void launch_slab_kernel<float>(const SlabParams<float>&, const CUtensorMap*, int, cudaStream_t);
 template void launch_slab_kernel<double>(const SlabParams<double>&, const CUtensorMap*, int, cudaStream_t);
-template void launch_finalize<float>(const FinalizeParams<float>&, int, cudaStream_t);
-template void launch_finalize<double>(const FinalizeParams<double>&, int, cudaStream_t);
+template void launch_finalize<float>(const FinalizeParams<float>&, int, cudaStream_t, bool);
+template void launch_finalize<double>(const FinalizeParams<double>&, int, cudaStream_t, bool);
 template void launch_pad_fill<float>(void*, const void*, const int*, long long, long long, cudaStream_t);
 template void launch_pad_fill<double>(void*, const void*, const int*, long long, long long, cudaStream_t);
 template int slab_kernel_occupancy<float>();

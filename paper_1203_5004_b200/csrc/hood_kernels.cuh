@@ -67,7 +67,7 @@ struct FinalizeParams {
 template <class S>
 void launch_slab_kernel(const SlabParams<S>& p, const CUtensorMap* tmap, int grid, cudaStream_t st);
 template <class S>
-void launch_finalize(const FinalizeParams<S>& p, int instances, cudaStream_t st);
+void launch_finalize(const FinalizeParams<S>& p, int instances, cudaStream_t st, bool pdl = false);
 template <class S>
 void launch_pad_fill(void* padded, const void* corners, const int* counts, long long n, long long L,
                      cudaStream_t st);

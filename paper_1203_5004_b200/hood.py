@@ -21,7 +21,7 @@ from dataclasses import dataclass, field
 from typing import Optional
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-SO = os.path.join(PKG, "lib", "libhood_b200.so")
+SO = os.environ.get("HOOD_B200_LIB") or os.path.join(PKG, "lib", "libhood_b200.so")  # override: experiments
 
 HOOD_OK = 0
 HOOD_ERR_INVALID_ARG = 1

@@ -16,7 +16,7 @@ from paper_1203_5004_b200 import workloads as W  # noqa: E402
 L = H.library()
 L.hood_internal_set_debug.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
 ctx = H.Context.get(0)
-trace = torch.zeros(1024 + 4 * 8192, dtype=torch.int64, device="cuda")
+trace = torch.zeros(1024 + 8 * 8192, dtype=torch.int64, device="cuda")
 flush = torch.empty(64 << 20, dtype=torch.int32, device="cuda")
 for lg in [int(a) for a in sys.argv[1:]] or [12, 16, 20, 22, 24]:
     n = 1 << lg
@@ -39,13 +39,34 @@ for lg in [int(a) for a in sys.argv[1:]] or [12, 16, 20, 22, 24]:
         t = trace[:64].cpu().tolist()
     print(f"log2n={lg}: event {a.elapsed_time(b)*1e3:7.1f} us; in-kernel: prologue done +{(t[2]-t[0])/1e3:6.1f} us, "
           f"last exit +{(t[1]-t[0])/1e3:6.1f} us")
-    w = trace[1024:].view(-1, 4).cpu()
-    w = w[w[:, 0] > 0]
+    w = trace[1024:1024 + 4 * 8192].view(-1, 4).cpu()
+    cyc = trace[1024 + 4 * 8192:].view(-1, 4).cpu()
+    keep = w[:, 0] > 0
+    w = w[keep]
+    cyc = cyc[keep]
     ent = (w[:, 0] - t[0]).double() / 1e3
     ext = (w[:, 1] - t[0]).double() / 1e3
     dur = ext - ent
     q = lambda v: " ".join(f"{float(v.quantile(x)):.1f}" for x in (0, 0.1, 0.5, 0.9, 1.0))
     print(f"   {len(w)} warps; entry q0/10/50/90/100: {q(ent)}; exit: {q(ext)}; duration: {q(dur)}")
+    cnt = w[:, 3]
+    if int(cnt.abs().sum()):
+        cand = (cnt >> 32).double(); edge = ((cnt >> 16) & 0xffff).double(); many = (cnt & 0xffff).double()
+        order = torch.argsort(dur)
+        print("   fastest (sm, us, cand, edge, many):", [(int(w[i, 2]), round(float(dur[i]), 1), int(cand[i]), int(edge[i]), int(many[i])) for i in order[:8]])
+        print("   slowest:", [(int(w[i, 2]), round(float(dur[i]), 1), int(cand[i]), int(edge[i]), int(many[i])) for i in order[-12:]])
+        c = torch.corrcoef(torch.stack([dur, cand]))[0, 1]
+        for nm, j in (("cand+many path", 0), ("flush", 1), ("land", 2)):
+            v = cyc[:, j].double() / 1965.0
+            print(f"   {nm}: mean {float(v.mean()):.1f} us/warp, corr with duration {float(torch.corrcoef(torch.stack([dur, v]))[0, 1]):.2f}; slowest warps: {[round(float(v[i]), 1) for i in order[-6:]]}")
+        print(f"   mean cand {float(cand.mean()):.1f} many {float(many.mean()):.2f} edge {float(edge.mean()):.2f}; corr(duration, cand) = {float(c):.2f}")
+        # duration by SM: mean over the SM's warps
+        import collections
+        bysm = collections.defaultdict(list)
+        for i in range(len(w)):
+            bysm[int(w[i, 2])].append(float(dur[i]))
+        means = sorted((sum(v) / len(v), k) for k, v in bysm.items())
+        print("   SM mean duration: fastest", [(k, round(m, 1)) for m, k in means[:5]], "slowest", [(k, round(m, 1)) for m, k in means[-5:]])
     import collections
     persm = collections.defaultdict(list)
     for i in range(len(w)):
