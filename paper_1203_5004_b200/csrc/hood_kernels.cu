@@ -1712,10 +1712,11 @@ __global__ void pad_fill_kernel(typename PointT<S>::V* padded, const typename Po
 // 16-byte chunks per lane per block (blocks of 2 KB for U = 4, 4 KB for
 // U = 8); selected once per process (HOOD_RING=<D><P><U>, e.g. 234, overrides
 // it for experiments).
-#define HOOD_RING_SHAPES(X) X(2, 3, 4) X(1, 2, 4) X(2, 2, 4) X(1, 2, 8) X(1, 3, 8) X(2, 2, 8)
-// measured best (B200, round 1): float2 (1, 2, 8), double2 (2, 2, 8)
+#define HOOD_RING_SHAPES(X) X(2, 3, 4) X(1, 2, 4) X(2, 2, 4) X(1, 1, 8) X(1, 2, 8) X(1, 3, 8) X(2, 2, 8)
+// measured best (B200, round 1): (1, 1, 8) for both storages -- one block of
+// lookahead, one in flight, 4 KB blocks (tools/gpu_sweep.sh)
 template <class S>
-constexpr int kRingDefault = sizeof(S) == 4 ? 128 : 228;
+constexpr int kRingDefault = 118;
 template <class S>
 static int ring_shape() {
   static int d = [] {
