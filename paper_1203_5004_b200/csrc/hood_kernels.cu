@@ -461,12 +461,14 @@ __device__ int chain_linear(V* X, int s, int cnt) {
 }
 
 // Fold m x-sorted survivors SB[0..m) into the running hood Hs[0..h) by
-// monotone-chain pushes (one lane).
+// monotone-chain pushes (one lane; oracle.cpp:7-20).  Inlined so both arrays
+// stay shared-memory accesses; the next survivor is fetched ahead of the pops.
 template <class V>
-__device__ __noinline__ long long fold_linear(const V* SB, int m, V* Hs, long long h) {
+__device__ __forceinline__ long long fold_linear(const V* SB, int m, V* Hs, long long h) {
   V h1 = h >= 1 ? Hs[h - 1] : V{}, h2 = h >= 2 ? Hs[h - 2] : V{};
+  V q = m > 0 ? SB[0] : V{};
   for (int i = 0; i < m; ++i) {
-    const V q = SB[i];
+    const V qn = i + 1 < m ? SB[i + 1] : V{};
     while (h >= 2 && !above(h2, h1, q)) {
       --h;
       h1 = h2;
@@ -476,6 +478,7 @@ __device__ __noinline__ long long fold_linear(const V* SB, int m, V* Hs, long lo
     ++h;
     h2 = h1;
     h1 = q;
+    q = qn;
   }
   return h;
 }
@@ -772,7 +775,7 @@ __global__ void __maxnreg__(HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams
   constexpr int EXT = 128;
   constexpr unsigned FULL = 0xffffffffu;
   static_assert(U == 4 || U == 8, "ring swizzle");
-  static_assert(NP <= PC && NP <= 32, "pending buffer");
+  static_assert(2 * NP <= PC && NP <= 32, "pending buffer");
 
   extern __shared__ unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1084,10 +1087,8 @@ __global__ void __maxnreg__(HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams
           sv = (bs + cl * NP + lane < n) && !(q.y < tau);
         }
         const unsigned sm = __ballot_sync(FULL, sv);
-        const int cnt = __popc(sm);
-        if (pend + cnt > PC) flush();
-        if (sv) PBf[pend + __popc(sm & below)] = q;
-        pend += cnt;
+        if (sv) PBf[pend + __popc(sm & below)] = q;  // room: pend <= PC - 2 NP here
+        pend += __popc(sm);
       }
     } else if (cm != 0) {
       // many runs (arc-like input) or an instance edge (exact per-point
@@ -1138,6 +1139,7 @@ __global__ void __maxnreg__(HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams
       }
     }
     HOOD_TOC(c_cand);
+    if (pend > PC - 2 * NP) flush();  // keeps room for two candidate runs
     runmax = fmax(runmax, wcur);
     // slide the window: the block after this one becomes current
     lmc = lmw[0];

@@ -13,6 +13,8 @@ timeout 600 ncu --set full --import-source on --clock-control none -k regex:ring
   python bench.py --config 2 --steps 1 --warmup 3 --no-e2e --cpu-seconds 0.1 > gpurun_out/ncu_ring_c2.log 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:ring_hull -s 2 -c 1 -o gpurun_out/prof_ring_c5 -f \
   python bench.py --config 5 --steps 1 --warmup 3 --no-e2e --cpu-seconds 0.1 > gpurun_out/ncu_ring_c5.log 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:ring_hull -s 2 -c 1 -o gpurun_out/prof_ring_c4 -f \
+  python bench.py --config 4 --steps 1 --warmup 3 --no-e2e --cpu-seconds 0.1 > gpurun_out/ncu_ring_c4.log 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:finalize -s 2 -c 1 -o gpurun_out/prof_fin_c2 -f \
   python bench.py --config 2 --steps 1 --warmup 3 --no-e2e --cpu-seconds 0.1 > gpurun_out/ncu_fin_c2.log 2>&1
 ls -la gpurun_out
