@@ -13,7 +13,7 @@ constexpr int kStages = 3;          // TMA pipeline depth per CTA
 constexpr int kTileBytes = kThreads * 128;
 constexpr int kHCap = 1024;         // running slab hull kept in smem up to this many corners
 constexpr int kMaxSlabsPerInstance = 2048;
-constexpr int kMinUnitBlocks = 8;   // ring kernel: blocks per unit at least
+constexpr int kMinUnitBlocks = 2;   // ring kernel: blocks per unit at least
 
 // First error of a build, encoded as key = index*2 + (x_not_increasing ? 1 : 0)
 // so one atomicMin keeps validate_points' order (hoodbuf.cpp:48-58: at the

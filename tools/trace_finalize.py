@@ -30,6 +30,6 @@ for rep in range(5):
     H.build_hood_async(pts, corners=corners, counts=counts)
     L.hood_internal_set_debug(ctx.handle, 0, None)
     torch.cuda.synchronize()
-    f = trace[7 * 64: 7 * 64 + 12].cpu().tolist()
+    f = trace[7 * 64: 7 * 64 + 14].cpu().tolist()
     print(f"config {cfg} 2^{log2n}: finalize phases (cycles)", [f[i + 1] - f[i] for i in range(6)],
-          "total", f[6] - f[0], "A", f[8], "C", f[9], "hull", int(counts[0]), "chain loop", f[11] - f[10], "pre", f[10] - f[4])
+          "total", f[6] - f[0], "A", f[8], "C", f[9], "hull", int(counts[0]), "hull step", f[11] - f[10])
