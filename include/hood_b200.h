@@ -95,6 +95,16 @@ int hood_merge_segments_f32(hood_ctx* ctx, const float* d_seg_pts, const int32_t
 int hood_merge_segments_f64(hood_ctx* ctx, const double* d_seg_pts, const int32_t* d_counts, int64_t G,
                             int64_t seg_stride, double* d_corners, int32_t* d_count, void* stream);
 
+/* One round of the reference round loop (driver.cpp:20-43, the per-round
+ * operator launch(match_and_merge_kernel), kernel.cpp:155-161): d_in holds n
+ * slots in HoodBuffer layout with blocks of d (each block: its hood's corners
+ * left-packed, then REMOTE = (10, 0)); d_out receives the buffer with blocks of
+ * 2d -- each the hood of two adjacent input blocks, REMOTE-padded.  d a power
+ * of two, n a multiple of 2d; d_in == d_out allowed.  Asynchronous on
+ * `stream`.  The per-round parity seam. */
+int hood_merge_round_f32(hood_ctx* ctx, const float* d_in, int64_t n, int64_t d, float* d_out, void* stream);
+int hood_merge_round_f64(hood_ctx* ctx, const double* d_in, int64_t n, int64_t d, double* d_out, void* stream);
+
 /* Synchronizes the stream of the last build and reports its first error. */
 int hood_last_error(hood_ctx* ctx, hood_error* out);
 

@@ -422,9 +422,51 @@ int merge_segments(hood_ctx* ctx, const S* seg_pts, const int* counts, long long
   return cudaGetLastError() == cudaSuccess ? HOOD_OK : HOOD_ERR_CUDA;
 }
 
+// One round of the reference loop on the GPU: REMOTE-padded blocks of d in,
+// blocks of 2d out (driver.cpp:20-43 with launch(match_and_merge_kernel),
+// kernel.cpp:155-161).  Each pair of adjacent block hoods is merged by the
+// finalize kernel (one CTA per pair), then padded again.
+template <class S>
+int merge_round(hood_ctx* ctx, const S* in, long long n, long long d, S* out, cudaStream_t st) {
+  using V = typename PointT<S>::V;
+  if (!ctx || !in || !out) return HOOD_ERR_INVALID_ARG;
+  if (d < 1 || (d & (d - 1)) != 0 || n < 2 * d || n % (2 * d) != 0) return HOOD_ERR_INVALID_ARG;
+  cudaSetDevice(ctx->device);
+  int rc;
+  if ((rc = ensure_ws(ctx, n / d))) return rc;
+  if (in != out &&
+      cudaMemcpyAsync(out, in, (size_t)n * sizeof(V), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    return HOOD_ERR_CUDA;
+  int* pair_counts = reinterpret_cast<int*>(ctx->seg_base);  // n/(2d) ints, workspace
+  launch_block_count<S>(out, n, d, ctx->seg_cnt, st);
+  FinalizeParams<S> f{};
+  f.out = out;
+  f.out_counts = pair_counts;
+  f.seg_cnt = ctx->seg_cnt;
+  f.seg_apt = nullptr;
+  f.seg_base = nullptr;
+  f.seg_stride = d;
+  f.slabs_per_inst = 2;
+  f.L = 2 * d;
+  f.fcap = (int)(32768 / sizeof(V));
+  launch_finalize<S>(f, (int)(n / (2 * d)), st);
+  launch_pad_fill<S>(out, out, pair_counts, n, 2 * d, st);
+  ctx->last_stream = st;
+  ctx->have_last = true;
+  ctx->last_launches = 3;
+  return cudaGetLastError() == cudaSuccess ? HOOD_OK : HOOD_ERR_CUDA;
+}
+
 }  // namespace
 
 extern "C" {
+
+int hood_merge_round_f32(hood_ctx* ctx, const float* d_in, int64_t n, int64_t d, float* d_out, void* stream) {
+  return merge_round<float>(ctx, d_in, n, d, d_out, reinterpret_cast<cudaStream_t>(stream));
+}
+int hood_merge_round_f64(hood_ctx* ctx, const double* d_in, int64_t n, int64_t d, double* d_out, void* stream) {
+  return merge_round<double>(ctx, d_in, n, d, d_out, reinterpret_cast<cudaStream_t>(stream));
+}
 
 int hood_create(hood_ctx** out, int device) {
   if (!out) return HOOD_ERR_INVALID_ARG;

@@ -1708,6 +1708,37 @@ __global__ void pad_fill_kernel(typename PointT<S>::V* padded, const typename Po
   }
 }
 
+// Corners of each d-slot block of a REMOTE-padded buffer: the leading slots
+// with x <= 1 (hoodbuf.cpp:87-92 block_corners; geom.hpp:18 is_remote).  One
+// warp per block, ballot over the slots.
+template <class S>
+__global__ void block_count_kernel(const typename PointT<S>::V* slots, long long n, long long d, int* counts) {
+  const int lane = threadIdx.x & 31;
+  const long long nb = n / d;
+  for (long long b = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nb;
+       b += ((long long)gridDim.x * blockDim.x) >> 5) {
+    long long c = d;
+    for (long long e0 = 0; e0 < d; e0 += 32) {
+      const long long e = e0 + lane;
+      const bool rem = e < d && slots[b * d + e].x > (S)1;
+      const unsigned m = __ballot_sync(0xffffffffu, rem);
+      if (m) {
+        c = e0 + __ffs(m) - 1;
+        break;
+      }
+    }
+    if (lane == 0) counts[b] = (int)c;
+  }
+}
+
+template <class S>
+void launch_block_count(const void* slots, long long n, long long d, int* counts, cudaStream_t st) {
+  using V = typename PointT<S>::V;
+  const long long warps = n / d;
+  const long long blocks = min((warps * 32 + 255) / 256, 148LL * 32);
+  block_count_kernel<S><<<(int)blocks, 256, 0, st>>>(reinterpret_cast<const V*>(slots), n, d, counts);
+}
+
 // ------------------------------------------------------------------ host side
 
 // Ring kernel shape: D blocks of lookahead, P blocks in flight per warp, U
@@ -1850,6 +1881,8 @@ template void launch_slab_kernel<float>(const SlabParams<float>&, const CUtensor
 template void launch_slab_kernel<double>(const SlabParams<double>&, const CUtensorMap*, int, cudaStream_t);
 template void launch_finalize<float>(const FinalizeParams<float>&, int, cudaStream_t, bool);
 template void launch_finalize<double>(const FinalizeParams<double>&, int, cudaStream_t, bool);
+template void launch_block_count<float>(const void*, long long, long long, int*, cudaStream_t);
+template void launch_block_count<double>(const void*, long long, long long, int*, cudaStream_t);
 template void launch_pad_fill<float>(void*, const void*, const int*, long long, long long, cudaStream_t);
 template void launch_pad_fill<double>(void*, const void*, const int*, long long, long long, cudaStream_t);
 template int slab_kernel_occupancy<float>();

@@ -72,6 +72,8 @@ template <class S>
 void launch_pad_fill(void* padded, const void* corners, const int* counts, long long n, long long L,
                      cudaStream_t st);
 template <class S>
+void launch_block_count(const void* slots, long long n, long long d, int* counts, cudaStream_t st);
+template <class S>
 int slab_kernel_occupancy();    // slab-kernel CTAs per SM
 template <class S>
 int instance_kernel_occupancy();  // instance-kernel CTAs per SM

@@ -36,7 +36,7 @@ EXPORTS = [
     "hood_create", "hood_destroy", "hood_reserve", "hood_build_f32", "hood_build_f64",
     "hood_build_host_f32", "hood_build_host_f64", "hood_merge_segments_f32", "hood_merge_segments_f64",
     "hood_last_error", "hood_last_launch_count", "hood_status_string", "hood_abi_version",
-    "hood_set_profile_events",
+    "hood_set_profile_events", "hood_merge_round_f32", "hood_merge_round_f64",
 ]
 
 
@@ -81,6 +81,8 @@ def library():
                 getattr(L, nm).argtypes = [p, p, i64, i64, p, p, u32]
             for nm in ("hood_merge_segments_f32", "hood_merge_segments_f64"):
                 getattr(L, nm).argtypes = [p, p, p, i64, i64, p, p, p]
+            for nm in ("hood_merge_round_f32", "hood_merge_round_f64"):
+                getattr(L, nm).argtypes = [p, p, i64, i64, p, p]
             L.hood_last_error.argtypes = [p, ctypes.POINTER(_Err)]
             L.hood_last_launch_count.argtypes = [p]
             L.hood_set_profile_events.argtypes = [p, p, p]
@@ -267,6 +269,26 @@ def merge_segments(seg_pts, seg_counts, out=None, out_count=None, stream=None):
     if rc:
         _raise(rc)
     return out, out_count
+
+
+def merge_round(slots, d: int, out=None, stream=None):
+    """One reference round on the GPU (driver.cpp:20-43, kernel.cpp:155-161):
+    slots (n, 2) in HoodBuffer layout with blocks of d -> blocks of 2d."""
+    import torch
+    if not isinstance(slots, torch.Tensor) or not slots.is_cuda or slots.dim() != 2 or slots.shape[1] != 2:
+        raise TypeError("slots must be a CUDA tensor of shape (n, 2)")
+    slots = slots.contiguous()
+    dev = slots.device.index if slots.device.index is not None else torch.cuda.current_device()
+    ctx = Context.get(dev)
+    if out is None:
+        out = torch.empty_like(slots)
+    if stream is None:
+        stream = torch.cuda.current_stream(slots.device)
+    fn = library().hood_merge_round_f64 if slots.dtype == torch.float64 else library().hood_merge_round_f32
+    rc = fn(ctx.handle, slots.data_ptr(), slots.shape[0], int(d), out.data_ptr(), ctypes.c_void_p(stream.cuda_stream))
+    if rc:
+        _raise(rc)
+    return out
 
 
 def round_schedule(n: int):

@@ -341,3 +341,47 @@ def test_sharded_build_on_device(oracle_mod):
         assert same(res.hull.cpu().numpy(), oracle_mod.upper_hull(W.arc(1 << 14)))
     finally:
         dist.destroy_process_group()
+
+
+def test_merge_round_reference_pairs(golden):
+    """hood_merge_round on the reference's random hood pairs
+    (make_random_hood_pair, acceptance.cpp:79) against match_and_merge_block's
+    merged windows (test_kernel.cpp:302-328), REMOTE padding included."""
+    P = golden("pairs.npz")
+    for d in sorted(set(int(x) for x in P["pq"][:, 0])):
+        idx = [t for t in range(P["pq"].shape[0]) if int(P["pq"][t, 0]) == d]
+        buf = np.concatenate([P["slots"][t][: 2 * d] for t in idx])
+        want = np.concatenate([P["merged"][t][: 2 * d] for t in idx])
+        got = H.merge_round(torch.as_tensor(buf).cuda(), d).cpu().numpy()
+        assert same(got, want), d
+
+
+def test_merge_round_reproduces_reference_rounds(golden):
+    """Every round of the reference round loop (driver.cpp:20-43) on the
+    acceptance sweep (acceptance.cpp:46-64): round r's input buffer -> the
+    reference's round-r output buffer, all 8 sets of a size in one call."""
+    A = golden("acceptance.npz")
+    for N in [4, 8, 16, 32, 64, 128, 256]:
+        pts, rounds = A[f"pts_{N}"], A[f"rounds_{N}"]
+        cur = pts.reshape(-1, 2)
+        for r in range(rounds.shape[1]):
+            d = 2 ** (r + 1)
+            got = H.merge_round(torch.as_tensor(np.ascontiguousarray(cur)).cuda(), d).cpu().numpy()
+            want = rounds[:, r].reshape(-1, 2)
+            assert same(got, want), (N, r)
+            cur = want
+
+
+def test_merge_round_float_storage_and_in_place(oracle_mod):
+    """float2 slots, in-place (d_in == d_out), chained over all rounds from
+    blocks of 2 up to one block: the last buffer holds the reference hull."""
+    p = W.grid_uniform(1 << 12, seed=21).astype(np.float32)
+    t = torch.as_tensor(p).cuda()
+    d = 2
+    while d < t.shape[0]:
+        H.merge_round(t, d, out=t)
+        d *= 2
+    h = oracle_mod.upper_hull(p.astype(np.float64))
+    got = t.cpu().numpy()
+    assert same(got[: len(h)], h)
+    assert np.all(got[len(h):, 0] == 10.0) and np.all(got[len(h):, 1] == 0.0)
