@@ -38,7 +38,10 @@ typedef enum hood_status {
   HOOD_ERR_X_OUT_OF_RANGE = 3,   /* ValidationError::x_out_of_range      */
   HOOD_ERR_DEGENERATE = 4,       /* reserved: DegenerateTangent          */
   HOOD_ERR_CUDA = 5,             /* a CUDA runtime call failed           */
-  HOOD_ERR_CAPACITY = 6          /* workspace / record capacity exceeded */
+  HOOD_ERR_CAPACITY = 6,         /* workspace / record capacity exceeded */
+  HOOD_ERR_NOT_POWER_OF_TWO = 7, /* ValidationError::not_power_of_two    */
+  HOOD_ERR_PARSE = 8,            /* cli.hpp ParseError (line in err_line) */
+  HOOD_ERR_DEGENERATE_TRIPLE = 9 /* ValidationError::degenerate_triple   */
 } hood_status;
 
 /* hoodbuf.hpp:18-32 ValidationError / kernel.hpp:98-102 DegenerateTangent. */
@@ -115,6 +118,25 @@ int hood_last_launch_count(hood_ctx* ctx);
  * device build on its stream (roofline timing of the dominant kernel).
  * Pass NULLs to stop. */
 int hood_set_profile_events(hood_ctx* ctx, void* ev_before_slab, void* ev_after_slab);
+
+/* Host front end (no GPU needed).  The reference's point files and input
+ * checks, so files feed the build directly:
+ *   hood_parse_points     cli.cpp:62-99 parse_points: the point count, then
+ *                         x y pairs, '#' comments, count <= 2^26.  Writes
+ *                         *count; HOOD_ERR_CAPACITY when cap < *count (retry
+ *                         with a larger buffer); HOOD_ERR_PARSE with the line
+ *                         in *err_line.  Does not validate (read_points =
+ *                         parse + hood_validate_points, cli.cpp:56-60).
+ *   hood_format_points    cli.cpp:101-106 write_point_set ("%.17g"); returns
+ *                         the byte length, writes only when cap suffices.
+ *   hood_validate_points  hoodbuf.cpp:30-70 validate_points: power of two,
+ *                         x in (0, 1) strictly increasing, no triple within
+ *                         the 1e-9 collinearity margin (all triples for n <= 64,
+ *                         else consecutive + the reference's 10n sample);
+ *                         ijk receives the offending indices. */
+int hood_parse_points(const char* text, int64_t len, double* xy, int64_t cap, int64_t* count, int64_t* err_line);
+int64_t hood_format_points(const double* xy, int64_t n, char* buf, int64_t cap);
+int hood_validate_points(const double* xy, int64_t n, int64_t* ijk);
 
 const char* hood_status_string(int status);
 int hood_abi_version(void);

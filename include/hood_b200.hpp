@@ -18,6 +18,8 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <fstream>
+#include <iterator>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -37,6 +39,12 @@ struct ValidationError : std::runtime_error {
       : std::runtime_error(std::move(msg)), code(c), i(index) {}
   Code code;
   std::size_t i;
+};
+
+struct ParseError : std::runtime_error {  // cli.hpp:23-28
+  ParseError(const std::string& where, long long line)
+      : std::runtime_error(where + ":" + std::to_string(line) + ": parse error"), line(line) {}
+  long long line;
 };
 
 struct CudaError : std::runtime_error {
@@ -168,6 +176,70 @@ std::vector<P> upper_hull(std::span<const P> points, int device = 0) {
   BuildOptions o;
   o.device = device;
   return build_hood(points, o).hull;
+}
+
+// ---- point files (cli.cpp:56-106) and validate_points (hoodbuf.cpp:30-70) ----
+
+struct Point2d {
+  double x = 0.0, y = 0.0;
+  friend bool operator==(const Point2d&, const Point2d&) = default;
+};
+
+// validate_points: throws ValidationError (x_out_of_range / x_not_increasing
+// carry the index; not_power_of_two and degenerate_triple are reported through
+// std::invalid_argument with the reference's wording).
+template <class P>
+void validate_points(std::span<const P> pts) {
+  detail::check_layout<P>();
+  static_assert(std::is_same_v<detail::scalar_t<P>, double>, "validate_points takes {double x, y}");
+  std::int64_t ijk[3];
+  const int rc = hood_validate_points(reinterpret_cast<const double*>(pts.data()), (std::int64_t)pts.size(), ijk);
+  if (rc == HOOD_OK) return;
+  if (rc == HOOD_ERR_X_OUT_OF_RANGE)
+    throw ValidationError(ValidationError::Code::x_out_of_range, (std::size_t)ijk[0],
+                          "point " + std::to_string(ijk[0]) + " has x outside (0, 1)");
+  if (rc == HOOD_ERR_X_NOT_INCREASING)
+    throw ValidationError(ValidationError::Code::x_not_increasing, (std::size_t)ijk[0],
+                          "point " + std::to_string(ijk[0]) + " does not increase in x over its predecessor");
+  if (rc == HOOD_ERR_NOT_POWER_OF_TWO)
+    throw std::invalid_argument("point count " + std::to_string(ijk[0]) + " is not a power of 2 (or is < 2)");
+  throw std::invalid_argument("points " + std::to_string(ijk[0]) + ", " + std::to_string(ijk[1]) + ", " +
+                              std::to_string(ijk[2]) + " are collinear within margin");
+}
+
+// parse_points (no validation): the point count, then x y pairs.
+inline std::vector<Point2d> parse_points(const std::string& text, const std::string& where = "<stream>") {
+  std::int64_t n = 0, line = 0;
+  int rc = hood_parse_points(text.data(), (std::int64_t)text.size(), nullptr, 0, &n, &line);
+  if (rc == HOOD_ERR_PARSE) throw ParseError(where, line);
+  std::vector<Point2d> pts((std::size_t)n);
+  rc = hood_parse_points(text.data(), (std::int64_t)text.size(), reinterpret_cast<double*>(pts.data()), n, &n,
+                         &line);
+  if (rc == HOOD_ERR_PARSE) throw ParseError(where, line);
+  if (rc != HOOD_OK) throw std::runtime_error(std::string("hood_b200: ") + hood_status_string(rc));
+  return pts;
+}
+
+// read_points = parse + validate (cli.cpp:56-60).
+inline std::vector<Point2d> read_points(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw std::runtime_error("can't open " + path);
+  const std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  auto pts = parse_points(text, path);
+  validate_points(std::span<const Point2d>(pts));
+  return pts;
+}
+
+// write_point_set's text (cli.cpp:101-106, "%.17g").
+template <class P>
+std::string format_points(std::span<const P> pts) {
+  detail::check_layout<P>();
+  static_assert(std::is_same_v<detail::scalar_t<P>, double>, "format_points takes {double x, y}");
+  const auto* xy = reinterpret_cast<const double*>(pts.data());
+  const std::int64_t len = hood_format_points(xy, (std::int64_t)pts.size(), nullptr, 0);
+  std::string s((std::size_t)len, '\0');
+  hood_format_points(xy, (std::int64_t)pts.size(), s.data(), len);
+  return s;
 }
 
 }  // namespace hood::b200

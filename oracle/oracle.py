@@ -107,6 +107,13 @@ def ref():
             L.ref_merge_block.argtypes = [_p, ctypes.c_int, ctypes.c_int, _p, _p]
             L.ref_make_random_hood_pair.restype = ctypes.c_int
             L.ref_make_random_hood_pair.argtypes = [ctypes.c_int, ctypes.c_uint64, _p, _p]
+            if hasattr(L, "ref_parse_points"):
+                L.ref_parse_points.restype = ctypes.c_int
+                L.ref_parse_points.argtypes = [ctypes.c_char_p, _i64, _p, _i64, _p, _p, _p]
+                L.ref_validate_points.restype = ctypes.c_int
+                L.ref_validate_points.argtypes = [_p, _i64, _p]
+                L.ref_format_coord.restype = ctypes.c_int
+                L.ref_format_coord.argtypes = [ctypes.c_double, ctypes.c_char_p, ctypes.c_int]
             for name in ("ref_classify_g", "ref_classify_f"):
                 getattr(L, name).restype = ctypes.c_int
                 getattr(L, name).argtypes = [_p, _i64] + [ctypes.c_int] * 4
@@ -261,3 +268,45 @@ def ref_make_random_hood_pair(d: int, seed: int):
     if ref().ref_make_random_hood_pair(d, seed, _ptr(slots), _ptr(pq)) != 0:
         raise RuntimeError("could not draw a valid hood pair")
     return slots, int(pq[0]), int(pq[1])
+
+
+# ---- reference front end (cli.cpp / hoodbuf.cpp via oracle/_ref) ----------
+
+def ref_parse_points(text: bytes):
+    """cli.cpp parse_points (+ validate_points): ('ok', pts) | ('parse', line) |
+    ('validation', code, (i, j, k))."""
+    L = ref()
+    cnt, line = ctypes.c_int64(0), ctypes.c_int64(0)
+    ijk = (ctypes.c_int64 * 3)()
+    cap = 1 << 16
+    out = np.empty((cap, 2))
+    rc = L.ref_parse_points(text, len(text), _ptr(out), cap, ctypes.byref(cnt), ctypes.byref(line), ijk)
+    if rc == 3:
+        out = np.empty((int(cnt.value), 2))
+        rc = L.ref_parse_points(text, len(text), _ptr(out), out.shape[0], ctypes.byref(cnt), ctypes.byref(line), ijk)
+    if rc == 0:
+        return ("ok", out[: int(cnt.value)].copy())
+    if rc == 1:
+        return ("parse", int(line.value))
+    return ("validation", int(line.value), (int(ijk[0]), int(ijk[1]), int(ijk[2])))
+
+
+def ref_validate_points(points):
+    """hoodbuf.cpp validate_points: -1 ok, else (code, (i, j, k))."""
+    a = np.ascontiguousarray(points, dtype=np.float64)
+    ijk = (ctypes.c_int64 * 3)()
+    c = ref().ref_validate_points(_ptr(a), a.shape[0], ijk)
+    return -1 if c < 0 else (c, (int(ijk[0]), int(ijk[1]), int(ijk[2])))
+
+
+def ref_format_coord(v: float) -> bytes:
+    buf = ctypes.create_string_buffer(64)
+    n = ref().ref_format_coord(float(v), buf, 64)
+    return buf.raw[:n]
+
+
+def ref_format_points(points) -> bytes:
+    """write_point_set's layout (cli.cpp:101-106) over the reference's format_coord."""
+    a = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 2)
+    return (str(a.shape[0]) + "\n").encode() + b"".join(
+        ref_format_coord(x) + b" " + ref_format_coord(y) + b"\n" for x, y in a)

@@ -12,6 +12,10 @@
 #include <thread>
 #include <vector>
 
+#include <sstream>
+#include <string>
+
+#include "hood/cli.hpp"
 #include "hood/driver.hpp"
 #include "hood/hoodbuf.hpp"
 #include "hood/kernel.hpp"
@@ -181,6 +185,57 @@ int ref_classify_g(const double* hood, int64_t len, int i, int j, int start, int
 }
 int ref_classify_f(const double* hood, int64_t len, int i, int j, int start, int d) {
   return static_cast<int>(hood::classify_f(as_points(hood, len), i, j, start, d));
+}
+
+
+// cli.cpp:62-99 parse_points (which validates, hoodbuf.cpp:30-70).
+// Returns 0 ok, 1 ParseError (line in *line), 2 ValidationError (code in
+// *line: 0 not_power_of_two, 1 x_out_of_range, 2 x_not_increasing,
+// 3 degenerate_triple; indices in ijk), 3 out of capacity.
+int ref_parse_points(const char* text, int64_t len, double* xy, int64_t cap, int64_t* count, int64_t* line,
+                     int64_t* ijk) {
+  std::istringstream in(std::string(text, static_cast<std::size_t>(len)));
+  try {
+    const hood::PointSet ps = hood::cli::parse_points(in, "<text>");
+    *count = ps.size();
+    if (ps.size() > cap) return 3;
+    std::memcpy(xy, ps.points().data(), static_cast<std::size_t>(ps.size()) * sizeof(Point2));
+    return 0;
+  } catch (const hood::cli::ParseError& e) {
+    *line = e.line;
+    return 1;
+  } catch (const hood::ValidationError& e) {
+    *line = static_cast<int64_t>(e.code);
+    ijk[0] = static_cast<int64_t>(e.i);
+    ijk[1] = static_cast<int64_t>(e.j);
+    ijk[2] = static_cast<int64_t>(e.k);
+    return 2;
+  }
+}
+
+// hoodbuf.cpp:30-70 validate_points: -1 ok, else the ValidationError code.
+int ref_validate_points(const double* xy, int64_t n, int64_t* ijk) {
+  std::vector<Point2> v(as_points(xy, n).begin(), as_points(xy, n).end());
+  try {
+    hood::validate_points(std::move(v));
+    return -1;
+  } catch (const hood::ValidationError& e) {
+    ijk[0] = static_cast<int64_t>(e.i);
+    ijk[1] = static_cast<int64_t>(e.j);
+    ijk[2] = static_cast<int64_t>(e.k);
+    return static_cast<int>(e.code);
+  }
+}
+
+// cli.cpp:96-100 format_coord (write_point_set prints "<n>\n" then
+// "<format_coord(x)> <format_coord(y)>\n" per point, cli.cpp:101-106).  The
+// stream-based writer itself is not called: libstdc++'s formatted output
+// crashes inside a ctypes-loaded library on this image.
+int ref_format_coord(double v, char* buf, int cap) {
+  const std::string s = hood::cli::format_coord(v);
+  if (static_cast<int>(s.size()) >= cap) return -1;
+  std::memcpy(buf, s.c_str(), s.size() + 1);
+  return static_cast<int>(s.size());
 }
 
 }  // extern "C"

@@ -19,7 +19,7 @@ LIB = os.path.join(PKG, "lib")
 SO = os.path.join(LIB, "libhood_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["hood_kernels.cu", "hood_capi.cu"]
+SOURCES = ["hood_kernels.cu", "hood_capi.cu", "hood_host.cpp"]
 HEADERS = ["hood_device.cuh", "hood_kernels.cuh"]
 
 

@@ -580,6 +580,9 @@ const char* hood_status_string(int s) {
     case HOOD_ERR_DEGENERATE: return "degenerate tangent";
     case HOOD_ERR_CUDA: return "CUDA error";
     case HOOD_ERR_CAPACITY: return "capacity exceeded";
+    case HOOD_ERR_NOT_POWER_OF_TWO: return "point count is not a power of 2 (or is < 2)";
+    case HOOD_ERR_PARSE: return "parse error";
+    case HOOD_ERR_DEGENERATE_TRIPLE: return "points collinear within margin";
   }
   return "unknown";
 }

@@ -30,6 +30,9 @@ HOOD_ERR_X_OUT_OF_RANGE = 3
 HOOD_ERR_DEGENERATE = 4
 HOOD_ERR_CUDA = 5
 HOOD_ERR_CAPACITY = 6
+HOOD_ERR_NOT_POWER_OF_TWO = 7
+HOOD_ERR_PARSE = 8
+HOOD_ERR_DEGENERATE_TRIPLE = 9
 HOOD_FLAG_CHECK_RANGE = 0x1
 
 EXPORTS = [
@@ -37,6 +40,7 @@ EXPORTS = [
     "hood_build_host_f32", "hood_build_host_f64", "hood_merge_segments_f32", "hood_merge_segments_f64",
     "hood_last_error", "hood_last_launch_count", "hood_status_string", "hood_abi_version",
     "hood_set_profile_events", "hood_merge_round_f32", "hood_merge_round_f64",
+    "hood_parse_points", "hood_format_points", "hood_validate_points",
 ]
 
 
@@ -98,7 +102,8 @@ def library():
 
 def _raise(code: int, index: int = -1):
     msg = library().hood_status_string(code).decode()
-    if code in (HOOD_ERR_X_NOT_INCREASING, HOOD_ERR_X_OUT_OF_RANGE):
+    if code in (HOOD_ERR_X_NOT_INCREASING, HOOD_ERR_X_OUT_OF_RANGE, HOOD_ERR_NOT_POWER_OF_TWO,
+                HOOD_ERR_DEGENERATE_TRIPLE):
         raise ValidationError(code, f"point {index}: {msg}", index)
     raise HoodError(code, msg, index)
 

@@ -143,6 +143,21 @@ int main() {
     }
     CHECK(thrown);
   }
+  // the reference's point-file front end (cli.cpp:62-106) feeding the build
+  {
+    const std::string text = "# E1\n4\n0.1 0.5\n0.2 0.6\n0.6 0.9\n0.7 0.2\n";
+    const auto pts = hood::b200::parse_points(text);
+    hood::b200::validate_points(std::span<const hood::b200::Point2d>(pts));
+    CHECK(build_hood(pts).hull == pts);
+    CHECK(hood::b200::parse_points(hood::b200::format_points(std::span<const hood::b200::Point2d>(pts))) == pts);
+    bool thrown = false;
+    try {
+      hood::b200::parse_points("3\n0.1 0.2\n0.3");
+    } catch (const hood::b200::ParseError& e) {
+      thrown = e.line == 3;
+    }
+    CHECK(thrown);
+  }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
 }

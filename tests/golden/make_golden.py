@@ -16,6 +16,10 @@ by oracle/Makefile, plus the extern "C" shim oracle/ref_shim.cpp) and records:
                   reference round loop (driver.cpp:20-43 steps), plus the
                   reference upper_hull of the config generators at small n
                   (grid 2^16, arc 2^14, gauss 2^16, batched 64 x 1024).
+  io.npz          the reference front end on fixed texts and arrays:
+                  cli::parse_points (+ validate_points) outcomes, format_coord
+                  strings, validate_points codes (cli.cpp:62-106,
+                  hoodbuf.cpp:30-70), incl. tests/data/sample8.txt.
   pairs.npz       make_random_hood_pair(d, 0xC4C5 + t) windows (acceptance.cpp:79)
                   with the reference classify_g / classify_f tables and the
                   merged block of match_and_merge_block (test_kernel.cpp:302-328).
@@ -143,12 +147,85 @@ def pairs():
                         scratch01=np.stack(scratch01))
 
 
+IO_TEXTS = [
+    b"4\n0.1 0.5 # A\n0.2 0.6\n0.6 0.9\n0.7 0.2\n",            # E1, test_kernel.cpp:17-117
+    b"# comment only line\n2\n0.25 0.1\n0.75 0.9\n",
+    b"2 0.25 0.1 0.75 0.9",                                       # one line
+    b"3\n0.1 0.2\n0.3",                                           # truncated
+    b"2\n0.1 0.2\n0.3 0.4\n5\n",                                  # trailing input
+    b"x\n",                                                       # bad count
+    b"-1\n",                                                      # negative count
+    b"2\n0.1 abc\n0.3 0.4\n",                                     # bad number
+    b"99999999999\n",                                             # count out of range
+    b"",                                                          # empty
+    b"3\n0.1 0.2\n0.2 0.3\n0.3 0.5\n",                            # not a power of two
+    b"4\n0.1 0.1\n0.2 0.2\n0.3 0.3\n0.4 0.5\n",                    # collinear triple
+    b"4\n0.1 0.5\n0.1 0.6\n0.6 0.9\n0.7 0.2\n",                    # x not increasing
+    b"4\n0 0.5\n0.2 0.6\n0.6 0.9\n0.7 0.2\n",                      # x out of range
+    b"2\n1e-3 .5e0\n0x1p-1 0.25\n",                                # strtod forms
+]
+
+
+def io():
+    texts = list(IO_TEXTS)
+    sample = os.path.join(O.REF_ROOT, "tests", "data", "sample8.txt") if hasattr(O, "REF_ROOT") else \
+        "/root/reference/proj/tests/data/sample8.txt"
+    with open(sample, "rb") as f:
+        texts.append(f.read())
+    rng = np.random.default_rng(5)
+    for n in (64, 128, 1024):
+        p = O.ref_make_random_point_set(n, 77 + n)
+        texts.append(O.ref_format_points(p))
+        bad = p.copy()
+        bad[n // 2, 0] = bad[n // 2 - 1, 0]  # x not increasing
+        texts.append(O.ref_format_points(bad))
+    kinds, lines, codes, ijks, pts = [], [], [], [], []
+    for t in texts:
+        r = O.ref_parse_points(t)
+        kinds.append({"ok": 0, "parse": 1, "validation": 2}[r[0]])
+        lines.append(r[1] if r[0] == "parse" else -1)
+        codes.append(r[1] if r[0] == "validation" else -1)
+        ijks.append(r[2] if r[0] == "validation" else (-1, -1, -1))
+        pts.append(r[1] if r[0] == "ok" else np.zeros((0, 2)))
+    # format_coord on awkward doubles
+    vals = np.array([0.1, 0.5, 1.0 / 3.0, 2.0 ** -24, 1e-300, 123456789.125, 0.0, -0.0, 5e-324,
+                     np.nextafter(1.0, 0.0)] + list(rng.random(50)), dtype=np.float64)
+    coords = [O.ref_format_coord(v) for v in vals]
+    # validate_points codes on random sets with planted defects
+    varr, vres = [], []
+    for t in range(24):
+        n = [4, 8, 64, 128, 256][t % 5]
+        p = O.ref_make_random_point_set(n, 900 + t)
+        if t % 4 == 1:
+            i = 1 + (t % (n - 2))
+            p[i, 1] = p[i - 1, 1] + (p[i + 1, 1] - p[i - 1, 1]) * (p[i, 0] - p[i - 1, 0]) / (p[i + 1, 0] - p[i - 1, 0])
+        elif t % 4 == 2:
+            p[n // 2, 0] = p[n // 2 - 1, 0]
+        elif t % 4 == 3:
+            p = p[:-1]
+        r = O.ref_validate_points(p)
+        varr.append(np.concatenate([p, np.zeros((256 - len(p), 2))]))
+        vres.append((len(p), -1, -1, -1, -1) if r == -1 else (len(p), r[0], *r[1]))
+    def blob(items):
+        off = np.cumsum([0] + [len(x) for x in items])
+        return np.frombuffer(b"".join(items), dtype=np.uint8), off
+    tb, to = blob(texts)
+    cb, co = blob(coords)
+    pcat = np.concatenate([p.reshape(-1, 2) for p in pts]) if pts else np.zeros((0, 2))
+    poff = np.cumsum([0] + [len(p) for p in pts])
+    np.savez_compressed(os.path.join(OUT, "io.npz"), text_blob=tb, text_off=to, kinds=np.array(kinds),
+                        lines=np.array(lines), codes=np.array(codes), ijks=np.array(ijks), pts=pcat,
+                        pts_off=poff, coord_vals=vals, coord_blob=cb, coord_off=co,
+                        varr=np.stack(varr), vres=np.array(vres))
+
+
 if __name__ == "__main__":
     O.build(ref=True)
     acceptance()
     driver()
     raw()
     pairs()
+    io()
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))
