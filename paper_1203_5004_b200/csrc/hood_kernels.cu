@@ -483,6 +483,41 @@ __device__ __forceinline__ long long fold_linear(const V* SB, int m, V* Hs, long
   return h;
 }
 
+// Strict upper hull of m <= 64 x-sorted points P[0..m) by the whole warp
+// (iterated pruning: a point not strictly above the chord of its alive
+// neighbours lies below the hull and is dropped, geom.hpp:22-28 predicate in
+// canonical order; when a round drops nothing the chain is strictly concave --
+// the set oracle.cpp:7-20 returns).  Writes the hull to dst (may alias P only
+// if dst == P), returns its size.  Latency ~rounds x one predicate instead of
+// one serial push per point.
+template <class V>
+__device__ __forceinline__ int warp_hull_small(const V* P, int m, V* dst) {
+  const int lane = threadIdx.x & 31;
+  const int i0 = lane, i1 = lane + 32;
+  const V q0 = i0 < m ? P[i0] : V{}, q1 = i1 < m ? P[i1] : V{};
+  unsigned long long alive = m >= 64 ? ~0ull : ((1ull << m) - 1ull);
+  auto keep = [&](int i, const V& q) -> bool {
+    if (!((alive >> i) & 1ull)) return false;
+    const unsigned long long lo = alive & ((1ull << i) - 1ull);
+    const unsigned long long hi = i == 63 ? 0ull : (alive & ~((2ull << i) - 1ull));
+    if (!lo || !hi) return true;  // the chain's ends stay
+    return above(P[63 - __clzll(lo)], q, P[__ffsll(hi) - 1]);
+  };
+  for (;;) {
+    const bool k0 = keep(i0, q0);
+    const bool k1 = m > 32 ? keep(i1, q1) : false;
+    const unsigned long long nxt = (unsigned long long)__ballot_sync(0xffffffffu, k0) |
+                                   ((unsigned long long)__ballot_sync(0xffffffffu, k1) << 32);
+    if (nxt == alive) break;
+    alive = nxt;
+  }
+  __syncwarp();
+  if ((alive >> i0) & 1ull) dst[__popcll(alive & ((1ull << i0) - 1ull))] = q0;
+  if (m > 32 && ((alive >> i1) & 1ull)) dst[__popcll(alive & ((1ull << i1) - 1ull))] = q1;
+  __syncwarp();
+  return __popcll(alive);
+}
+
 // Many survivors (arc-like input, an instance edge): the warp hulls 32 runs
 // of SB in parallel, merges them with a warp merge tree and bridges the block
 // hood into the running hood (spilling it to HBM when it outgrows Hs).
@@ -1155,7 +1190,14 @@ __global__ void __maxnreg__(HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams
 
     if (nrem == 0) {
       // unit done: its hood to the output slots, its summary for finalize
-      flush();
+      if (hs.in_smem && hs.n == 0 && pend <= PC) {
+        // the whole unit's survivors are still queued (short units, batched
+        // instances): hull them with the warp, straight into the output slots
+        hs.n = pend ? warp_hull_small<V>(PBf, pend, Hs) : 0;
+        pend = 0;
+      } else {
+        flush();
+      }
       if (hs.in_smem)
         for (long long e = lane; e < hs.n; e += 32) gout[ubase + e] = Hs[e];
       if (spi > 1) {
