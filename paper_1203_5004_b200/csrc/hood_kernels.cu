@@ -1087,9 +1087,14 @@ __global__ void __maxnreg__(HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams
       inst = spi == 1 ? (int)u : (int)u / spi;
       ubase = (long long)cc.b * BP;
       // edge anchors: max y of up to EXT points on each side of the unit
-      if (cc.r != 0) ext_partial(cc.b, cc.e, pre_l, pre_r);
-      ext_l = __any_sync(FULL, pre_l != NEG) ? warp_max(pre_l) : NEG;
-      ext_r = __any_sync(FULL, pre_r != NEG) ? warp_max(pre_r) : NEG;
+      // (none when units are whole instances)
+      if (spi == 1) {
+        ext_l = ext_r = NEG;
+      } else {
+        if (cc.r != 0) ext_partial(cc.b, cc.e, pre_l, pre_r);
+        ext_l = __any_sync(FULL, pre_l != NEG) ? warp_max(pre_l) : NEG;
+        ext_r = __any_sync(FULL, pre_r != NEG) ? warp_max(pre_r) : NEG;
+      }
       runmax = ext_l;
       hs = HoodState{0, 1};
       pend = 0;

@@ -1,7 +1,7 @@
 """In-kernel timeline of the ring kernel (globaltimer): first warp entry, last
 prologue end, last warp exit, against the event-measured kernel time.
 
-  python tools/trace_ring.py [log2n ...]
+  python tools/trace_ring.py [log2n ... | b (batched 65536 x 1024) | g<log2n> (Gaussian double)]
 """
 import ctypes
 import os
@@ -18,11 +18,17 @@ L.hood_internal_set_debug.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_vo
 ctx = H.Context.get(0)
 trace = torch.zeros(1024 + 8 * 8192, dtype=torch.int64, device="cuda")
 flush = torch.empty(64 << 20, dtype=torch.int32, device="cuda")
-for lg in [int(a) for a in sys.argv[1:]] or [12, 16, 20, 22, 24]:
-    n = 1 << lg
-    pts = W.grid_uniform_torch(n, seed=2)
+for lg in sys.argv[1:] or ["12", "16", "20", "22", "24"]:
+    block = 0
+    if lg == "b":
+        pts, block = W.batched_torch(65536, 1024, seed=5), 1024
+    elif lg.startswith("g"):
+        pts = W.gauss_torch(1 << int(lg[1:]), seed=4)
+    else:
+        pts = W.grid_uniform_torch(1 << int(lg), seed=2)
+    n = pts.shape[0]
     corners = torch.empty_like(pts)
-    counts = torch.empty(1, dtype=torch.int32, device="cuda")
+    counts = torch.empty(max(n // block, 1) if block else 1, dtype=torch.int32, device="cuda")
     for rep in range(4):
         trace.zero_()
         trace[0] = (1 << 63) - 1
@@ -32,7 +38,7 @@ for lg in [int(a) for a in sys.argv[1:]] or [12, 16, 20, 22, 24]:
             e.record()
         L.hood_internal_set_debug(ctx.handle, 0, trace.data_ptr())
         ctx.set_profile_events(a, b)
-        H.build_hood_async(pts, corners=corners, counts=counts)
+        H.build_hood_async(pts, block, corners=corners, counts=counts)
         ctx.set_profile_events(None, None)
         L.hood_internal_set_debug(ctx.handle, 0, None)
         torch.cuda.synchronize()
