@@ -807,7 +807,7 @@ __global__ void __maxnreg__(HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams
   constexpr int BB = (int)LY::BB;
   constexpr int HC = HCap<S>::value;
   constexpr int PC = LY::PC;
-  constexpr int EXT = 128;
+  constexpr int EXT = 512;
   constexpr unsigned FULL = 0xffffffffu;
   static_assert(U == 4 || U == 8, "ring swizzle");
   static_assert(2 * NP <= PC && NP <= 32, "pending buffer");
