@@ -527,6 +527,32 @@ __device__ __noinline__ HoodState merge_block_tree(typename PointT<S>::V* SB, in
                                                    HoodState h) {
   using V = typename PointT<S>::V;
   const int lane = threadIdx.x & 31;
+  // concave fast path (arc-like input): if SB is a strictly concave chain that
+  // joins the hood without a pop -- the triples the monotone chain
+  // (oracle.cpp:7-20) would test, all strictly left -- it is appended as is
+  {
+    bool conc = true;
+    for (int i = 1 + lane; i + 1 < m; i += 32) conc = conc && above(SB[i - 1], SB[i], SB[i + 1]);
+    if (__all_sync(0xffffffffu, conc)) {
+      bool join = true;
+      if (lane == 0 && m >= 2) {
+        const V* hsrc = h.in_smem ? Hs : gslab;
+        if (h.n >= 2) join = above(hsrc[h.n - 2], hsrc[h.n - 1], SB[0]);
+        if (join && h.n >= 1) join = above(hsrc[h.n - 1], SB[0], SB[1]);
+      }
+      if (m >= 2 && __shfl_sync(0xffffffffu, join, 0)) {
+        if (h.in_smem && h.n + m > HC) {  // spill the hood to the output slots
+          for (long long i = lane; i < h.n; i += 32) gslab[i] = Hs[i];
+          h.in_smem = 0;
+        }
+        V* dstp = h.in_smem ? Hs : gslab;
+        for (int i = lane; i < m; i += 32) dstp[h.n + i] = SB[i];
+        __syncwarp();
+        h.n += m;
+        return h;
+      }
+    }
+  }
   const int ch = (m + 31) / 32;
   const int s = min(m, lane * ch), e = min(m, s + ch);
   const int cnt = chain_linear(SB, s, e - s);
