@@ -1710,10 +1710,18 @@ __global__ void __launch_bounds__(kFinThreads, 1) finalize_kernel(const Finalize
     }
   }
 
-  // huge hoods (the arc, many candidates): merge tree over the slab hoods in
-  // place in HBM; every slab keeps its run strictly above its chord A-C
-  // (found with binary searches: the run is contiguous and the height above
-  // the chord is unimodal along the hood)
+  // huge hoods (the arc, many candidates): every slab keeps its run strictly
+  // above its chord A-C (found with binary searches: the run is contiguous and
+  // the height above the chord is unimodal along the hood).  The ends of the
+  // thread's slabs are loaded up front so the checks overlap.
+  V e0[R], e1[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const int s = tid * per + j;
+    const bool live = j < per && s < M && sc[j] > 0;
+    e0[j] = live ? gout[sb[j]] : NOPT;
+    e1[j] = live ? gout[sb[j] + sc[j] - 1] : NOPT;
+  }
 #pragma unroll
   for (int j = 0; j < R; ++j) {
     const int s = tid * per + j;
@@ -1722,7 +1730,7 @@ __global__ void __launch_bounds__(kFinThreads, 1) finalize_kernel(const Finalize
       const V A = aA[j], Cp = aC[j];
       const V* h = gout + sb[j];
       const int c = sc[j];
-      if (c > 0 && A.y > NEG && Cp.y > NEG && !(above(A, h[0], Cp) && above(A, h[c - 1], Cp))) {
+      if (c > 0 && A.y > NEG && Cp.y > NEG && !(above(A, e0[j], Cp) && above(A, e1[j], Cp))) {
         int a = 0, bq = c - 1;
         while (a < bq) {
           const int mid = (a + bq) >> 1;
@@ -1755,16 +1763,75 @@ __global__ void __launch_bounds__(kFinThreads, 1) finalize_kernel(const Finalize
     }
   }
   __syncthreads();
+  if (p.trace && tid == 0) p.trace[20] = clock64();
+  // concatenation fast path (arc-like slabs): when every slab kept a run and
+  // every junction is convex -- the triples the monotone chain would test at
+  // the seams, all strictly left -- the hood is the runs in order
+  int ok = 1, tot = 0;
+  {
+    int mine = 0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int s = tid * per + j;
+      if (j < per && s < M) {
+        const int m = ncd[s];
+        mine += m;
+        if (m == 0 || (m == 1 && s > 0 && s + 1 < M)) {
+          ok = 0;  // an empty or single-point run: the seams need the merge tree
+        } else if (s + 1 < M) {
+          const int k = ncd[s + 1];
+          if (k == 0) {
+            ok = 0;
+          } else {
+            const V* P = gout + nsd[s];
+            const V* Q = gout + nsd[s + 1];
+            if (m >= 2) ok &= above(P[m - 2], P[m - 1], Q[0]);
+            if (ok && k >= 2) ok &= above(P[m - 1], Q[0], Q[1]);
+          }
+        }
+      }
+    }
+    ok = __syncthreads_and(ok);
+    if (ok) {
+      const int off = block_excl_sum<NWP>(mine, shI, &tot);
+      // in place when every run already sits at its offset (full slabs)
+      int inplace = 1, o = off;
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const int s = tid * per + j;
+        if (j < per && s < M) {
+          inplace &= nsd[s] == ibase + o;
+          o += ncd[s];
+        }
+      }
+      inplace = __syncthreads_and(inplace);
+      if (!inplace) ok = 0;  // general compaction: leave it to the merge tree
+    }
+  }
+  if (ok) {
+    if (tid == 0) p.out_counts[blockIdx.x] = tot;
+    if (p.trace && tid == 0) p.trace[21] = clock64();
+    return;
+  }
   int levels = 0;
   while ((1 << levels) < M) ++levels;
   tree_merge<V>(PtrAcc<V>{gout}, nsd, ncd, M, levels);
-  if (tid == 0) {
-    const long long st = nsd[0];
-    const int hc = ncd[0];
-    if (st != ibase)
-      for (int e = 0; e < hc; ++e) gout[ibase + e] = gout[st + e];
-    p.out_counts[blockIdx.x] = hc;
+  if (p.trace && tid == 0) p.trace[21] = clock64();
+  // the merged hood to the instance's first slots: a forward copy in chunks
+  // (every chunk is read before it is written, destination below source)
+  const long long st = nsd[0];
+  const int hc = ncd[0];
+  __syncthreads();
+  if (st != ibase) {
+    for (int c0 = 0; c0 < hc; c0 += kFinThreads) {
+      const int e = c0 + tid;
+      const V v = e < hc ? gout[st + e] : NOPT;
+      __syncthreads();
+      if (e < hc) gout[ibase + e] = v;
+      __syncthreads();
+    }
   }
+  if (tid == 0) p.out_counts[blockIdx.x] = hc;
 }
 
 // ------------------------------------------------------------------ padding
