@@ -253,7 +253,10 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    # the multi-GPU path (NCCL exchange of slab hoods); HOOD_BENCH_DIST=1
+    # exercises it on a single GPU (torchrun --nproc-per-node 1)
+    multi = world > 1 or os.environ.get("HOOD_BENCH_DIST") == "1"
+    if multi:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
@@ -282,35 +285,37 @@ def run_ours(args):
 
     # multi-GPU exchange buffers (slab hoods in global double coordinates)
     CAP = 4096
-    if world > 1:
+    # batched instances (config 5) are independent objects: no exchange
+    exchange_slabs = multi and not block
+    if exchange_slabs:
         rec = torch.zeros(CAP + 1, 2, dtype=torch.float64, device=dev)
         gathered = torch.zeros(world, CAP + 1, 2, dtype=torch.float64, device=dev)
-        seg_cnt = torch.zeros(world, dtype=torch.int32, device=dev)
         final = torch.empty(world * CAP, 2, dtype=torch.float64, device=dev)
         final_cnt = torch.empty(1, dtype=torch.int32, device=dev)
 
     def exchange():
-        # slab r lives at x in (r, r+1): shift the (float) slab hood into
-        # global double coordinates (exact), gather, merge on every rank.
-        k = counts[0]
-        idx = torch.arange(CAP, device=dev)
-        h = corners[:CAP].to(torch.float64)
-        h[:, 0] += rank
-        rec[1:] = torch.where((idx < k)[:, None], h, torch.zeros_like(h))
-        rec[0, 0] = k.to(torch.float64)
+        # slab r lives at x in (r, r+1): its hood goes into global double
+        # coordinates (exact) in one pack kernel, the records are gathered
+        # over NCCL, and every rank merges them (paper_1203_5004_b200/distributed.py)
+        H.pack_record(corners, counts, CAP, x_offset=float(rank), rec=rec)
         dist.all_gather_into_tensor(gathered.view(-1), rec.view(-1))
-        seg_cnt.copy_(gathered[:, 0, 0].to(torch.int32))
-        H.merge_segments(gathered[:, 1:, :].contiguous(), seg_cnt, out=final, out_count=final_cnt)
+        H.merge_records(gathered, out=final, out_count=final_cnt)
+
+    step_launches = [0]
 
     def one_step():
         H.build_hood_async(pts, block, corners=corners, counts=counts)
-        if world > 1:
+        k = ctx.last_launch_count()
+        if exchange_slabs:
             exchange()
+            k += ctx.last_launch_count()
+        step_launches[0] = k
 
-    # correctness gate before timing (one build vs the CPU oracle on rank 0)
+    # first build outside the timing: surfaces validation errors (and record
+    # overflow of the exchange) before anything is timed
     one_step()
     ctx.last_error()
-    if world > 1 and int(counts[0]) > CAP:
+    if exchange_slabs and int(counts[0]) > CAP:
         raise RuntimeError("slab hood exceeds the exchange record capacity")
 
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -329,11 +334,13 @@ def run_ours(args):
     # microseconds of step time, so they stay out of the timed steps).
     # Multi-GPU steps (NCCL exchange) run eagerly.
     graph = prof_graph = None
-    if world == 1:
+    if not multi or os.environ.get("HOOD_BENCH_EAGER") != "1":
+        # multi-GPU steps are captured too: the NCCL all-gather and the merge
+        # are graph-safe, so a step is one replay on every rank
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             one_step()
-        launches_per_step = ctx.last_launch_count()
+        launches_per_step = step_launches[0]
         step = graph.replay
         if not args.no_kernel_events:
             ctx.set_profile_events(kb, ka)
@@ -351,7 +358,7 @@ def run_ours(args):
             flush_l2()
             prof_graph.replay()
     torch.cuda.synchronize()
-    if world > 1:
+    if multi:
         dist.barrier()
     torch.cuda.synchronize()
     launches = 0
@@ -362,9 +369,9 @@ def run_ours(args):
             ev0[i].record(stream)
             step()
             ev1[i].record(stream)
-            launches += (launches_per_step if launches_per_step is not None else ctx.last_launch_count() + 1)
+            launches += launches_per_step if launches_per_step is not None else step_launches[0]
         torch.cuda.synchronize()
-    if world > 1:
+    if multi:
         dist.barrier()
     torch.cuda.synchronize()
     # roofline pass: the slab kernel alone, event-timed on its own stream
@@ -383,12 +390,12 @@ def run_ours(args):
     else:
         kern_ms.append(float("nan"))
     torch.cuda.synchronize()
-    if world > 1:
+    if multi:
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
     ms = statistics.mean(step_ms)
     kms = statistics.mean(kern_ms)
-    if world > 1:
+    if multi:
         t = torch.tensor([ms, kms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, kms = float(t[0]), float(t[1])
@@ -402,13 +409,13 @@ def run_ours(args):
         cnt_h = torch.zeros(inst, dtype=torch.int32).pin_memory()
         e_times = []
         for i in range(args.warmup + args.steps):
-            if world > 1:
+            if multi:
                 dist.barrier()
             t0 = time.perf_counter()
             rc = H.build_hood_host_ptr(ctx, host.data_ptr(), n, f64, out_h.data_ptr(), cnt_h.data_ptr(), block)
             if rc:
                 raise RuntimeError(f"host build failed: {rc}")
-            if world > 1:
+            if exchange_slabs:
                 corners[: int(cnt_h[0])].copy_(out_h[: int(cnt_h[0])], non_blocking=True)
                 counts[0] = int(cnt_h[0])
                 exchange()
@@ -416,7 +423,7 @@ def run_ours(args):
             if i >= args.warmup:
                 e_times.append(time.perf_counter() - t0)
         e_ms = statistics.mean(e_times) * 1e3
-        if world > 1:
+        if multi:
             t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t[0])
@@ -448,10 +455,11 @@ def run_ours(args):
             "config": {"workload": desc, "n_per_rank": n, "storage": storage, "bytes_per_point": bpp,
                        "block_len": block or n, "l2": "flushed between timed steps (256 MiB write, then 256 MiB read of another buffer)",
                        "predicate": "reference double orient, certified f32 filter",
-                       "parallelism": f"x-slab dp{world}" if world > 1 else "single GPU"},
+                       "parallelism": (f"x-slab dp{world}, NCCL all-gather of slab hoods + merge" if exchange_slabs
+                                       else f"{world} GPUs, independent instances" if multi else "single GPU")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(args.config),
-                         "kernel": "slab_hull_kernel", "kernel_ms": kms,
+                         "kernel": "ring_hull_kernel", "kernel_ms": kms,
                          "algorithmic_bytes_per_launch": n * bpp, "peak_source": peak_src},
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -460,7 +468,7 @@ def run_ours(args):
             "impl": "ours",
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if multi:
         dist.barrier()
         dist.destroy_process_group()
     return 0

@@ -98,6 +98,19 @@ int hood_merge_segments_f32(hood_ctx* ctx, const float* d_seg_pts, const int32_t
 int hood_merge_segments_f64(hood_ctx* ctx, const double* d_seg_pts, const int32_t* d_counts, int64_t G,
                             int64_t seg_stride, double* d_corners, int32_t* d_count, void* stream);
 
+/* Multi-GPU exchange (the one collective of the x-slab sharding): each rank
+ * packs its slab hood into a record of cap+1 double2 -- header (count, 0),
+ * then the corners widened to double with x + x_offset -- the records are
+ * all-gathered (NCCL), and every rank merges the G records (rank order = x
+ * order) into the global hood: d_out (G*cap double2 slots) and d_count.
+ * Asynchronous, graph-capturable. */
+int hood_pack_record_f32(hood_ctx* ctx, const float* d_corners, const int32_t* d_count, int64_t cap,
+                         double x_offset, double* d_rec, void* stream);
+int hood_pack_record_f64(hood_ctx* ctx, const double* d_corners, const int32_t* d_count, int64_t cap,
+                         double x_offset, double* d_rec, void* stream);
+int hood_merge_records(hood_ctx* ctx, const double* d_recs, int64_t G, int64_t cap, double* d_out,
+                       int32_t* d_count, void* stream);
+
 /* One round of the reference round loop (driver.cpp:20-43, the per-round
  * operator launch(match_and_merge_kernel), kernel.cpp:155-161): d_in holds n
  * slots in HoodBuffer layout with blocks of d (each block: its hood's corners

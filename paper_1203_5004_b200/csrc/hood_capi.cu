@@ -30,9 +30,9 @@ struct hood_ctx {
   int* seg_cnt = nullptr;
   void* seg_apt = nullptr;  // double2-sized slots (fits float2 too)
   long long* seg_base = nullptr;
-  unsigned* pub = nullptr;
   long long seg_cap = 0;
   DevError* err = nullptr;
+  int* done = nullptr;      // merge_records: result already written by the gather kernel
   // host-path buffers
   void* d_in = nullptr;
   size_t d_in_bytes = 0;
@@ -124,17 +124,16 @@ int make_plan(hood_ctx* ctx, long long n, long long block_len, Plan& pl) {
 int ensure_ws(hood_ctx* ctx, long long slabs) {
   if (!ctx->err) {
     if (cudaMalloc(&ctx->err, sizeof(DevError)) != cudaSuccess) return HOOD_ERR_CUDA;
+    if (cudaMalloc(&ctx->done, sizeof(int)) != cudaSuccess) return HOOD_ERR_CUDA;
   }
   if (slabs > ctx->seg_cap) {
     cudaFree(ctx->seg_cnt);
     cudaFree(ctx->seg_apt);
     cudaFree(ctx->seg_base);
-    cudaFree(ctx->pub);
     const long long cap = std::max(slabs, 4096LL);
     if (cudaMalloc(&ctx->seg_cnt, cap * sizeof(int)) != cudaSuccess ||
         cudaMalloc(&ctx->seg_apt, cap * 2 * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&ctx->seg_base, cap * sizeof(long long)) != cudaSuccess ||
-        cudaMalloc(&ctx->pub, cap * sizeof(unsigned)) != cudaSuccess)
+        cudaMalloc(&ctx->seg_base, cap * sizeof(long long)) != cudaSuccess)
       return HOOD_ERR_CUDA;
     ctx->seg_cap = cap;
   }
@@ -188,7 +187,6 @@ SlabParams<S> slab_params(hood_ctx* ctx, const Plan& pl, const void* pts, void* 
   p.dbg = ctx->dbg;
   p.trace = ctx->trace;
   p.read_lim = pl.n;
-  p.pub = ctx->pub;
   return p;
 }
 
@@ -457,9 +455,63 @@ int merge_round(hood_ctx* ctx, const S* in, long long n, long long d, S* out, cu
   return cudaGetLastError() == cudaSuccess ? HOOD_OK : HOOD_ERR_CUDA;
 }
 
+// Multi-GPU exchange: pack this rank's slab hood into a
+// record; merge the G gathered records into the global hood.
+template <class S>
+int pack_record(hood_ctx* ctx, const S* corners, const int* count, long long cap, double x_offset, double* rec,
+                cudaStream_t st) {
+  if (!ctx || !corners || !count || !rec || cap < 1) return HOOD_ERR_INVALID_ARG;
+  cudaSetDevice(ctx->device);
+  launch_pack_record<S>(corners, count, cap, x_offset, rec, st);
+  ctx->last_stream = st;
+  ctx->have_last = true;
+  ctx->last_launches = 1;
+  return cudaGetLastError() == cudaSuccess ? HOOD_OK : HOOD_ERR_CUDA;
+}
+
+int merge_records(hood_ctx* ctx, const double* recs, long long G, long long cap, double* out, int* count,
+                  cudaStream_t st) {
+  if (!ctx || !recs || !out || !count || cap < 1) return HOOD_ERR_INVALID_ARG;
+  if (G < 1 || G > kMaxSlabsPerInstance) return HOOD_ERR_INVALID_ARG;
+  cudaSetDevice(ctx->device);
+  int rc;
+  if ((rc = ensure_ws(ctx, G))) return rc;
+  cudaMemsetAsync(ctx->err, 0xff, sizeof(DevError), st);
+  launch_gather_records(recs, G, cap, out, ctx->seg_cnt, count, ctx->done, st);
+  FinalizeParams<double> f{};
+  f.out = out;
+  f.out_counts = count;
+  f.seg_cnt = ctx->seg_cnt;
+  f.seg_apt = nullptr;
+  f.seg_base = nullptr;
+  f.seg_stride = cap;
+  f.slabs_per_inst = (int)G;
+  f.L = G * cap;
+  f.fcap = (int)(32768 / sizeof(double2));
+  f.done = ctx->done;
+  launch_finalize<double>(f, 1, st);
+  ctx->last_stream = st;
+  ctx->have_last = true;
+  ctx->last_launches = 2;
+  return cudaGetLastError() == cudaSuccess ? HOOD_OK : HOOD_ERR_CUDA;
+}
+
 }  // namespace
 
 extern "C" {
+
+int hood_pack_record_f32(hood_ctx* ctx, const float* d_corners, const int32_t* d_count, int64_t cap,
+                         double x_offset, double* d_rec, void* stream) {
+  return pack_record<float>(ctx, d_corners, d_count, cap, x_offset, d_rec, reinterpret_cast<cudaStream_t>(stream));
+}
+int hood_pack_record_f64(hood_ctx* ctx, const double* d_corners, const int32_t* d_count, int64_t cap,
+                         double x_offset, double* d_rec, void* stream) {
+  return pack_record<double>(ctx, d_corners, d_count, cap, x_offset, d_rec, reinterpret_cast<cudaStream_t>(stream));
+}
+int hood_merge_records(hood_ctx* ctx, const double* d_recs, int64_t G, int64_t cap, double* d_out, int32_t* d_count,
+                       void* stream) {
+  return merge_records(ctx, d_recs, G, cap, d_out, d_count, reinterpret_cast<cudaStream_t>(stream));
+}
 
 int hood_merge_round_f32(hood_ctx* ctx, const float* d_in, int64_t n, int64_t d, float* d_out, void* stream) {
   return merge_round<float>(ctx, d_in, n, d, d_out, reinterpret_cast<cudaStream_t>(stream));
@@ -491,8 +543,8 @@ int hood_destroy(hood_ctx* c) {
   cudaFree(c->seg_cnt);
   cudaFree(c->seg_apt);
   cudaFree(c->seg_base);
-  cudaFree(c->pub);
   cudaFree(c->err);
+  cudaFree(c->done);
   cudaFree(c->d_in);
   cudaFree(c->d_out);
   cudaFree(c->d_counts);

@@ -1559,7 +1559,11 @@ __global__ void __launch_bounds__(kFinThreads, 1) finalize_kernel(const Finalize
   V* F = reinterpret_cast<V*>(smem_raw + o_stg + (size_t)MAXC * CAP * sizeof(double2));  // [2][fcap]
 
   asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the slab kernel has completed
-  if (p.trace && tid == 0) p.trace[0] = clock64();
+  if (p.done && *p.done) return;  // merged already (small exchange)
+  if (p.trace && tid == 0) {
+    p.trace[0] = clock64();
+    p.trace[30] = (long long)gtimer();
+  }
   const int per = (M + kFinThreads - 1) / kFinThreads;
   long long sb[R];
   int sc[R];
@@ -1879,6 +1883,76 @@ void launch_block_count(const void* slots, long long n, long long d, int* counts
   block_count_kernel<S><<<(int)blocks, 256, 0, st>>>(reinterpret_cast<const V*>(slots), n, d, counts);
 }
 
+// Exchange record of one rank's slab hood: header (count, 0),
+// then the corners widened to double with x shifted into global coordinates.
+template <class S>
+__global__ void pack_record_kernel(const typename PointT<S>::V* corners, const int* count, long long cap,
+                                   double x_offset, double2* rec) {
+  const long long k = min((long long)*count, cap);
+  if (blockIdx.x == 0 && threadIdx.x == 0) rec[0] = make_double2((double)*count, 0.0);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += (long long)gridDim.x * blockDim.x) {
+    const typename PointT<S>::V c = corners[i];
+    rec[1 + i] = make_double2((double)c.x + x_offset, (double)c.y);
+  }
+}
+
+template <class S>
+void launch_pack_record(const void* corners, const int* count, long long cap, double x_offset, double* rec,
+                        cudaStream_t st) {
+  using V = typename PointT<S>::V;
+  pack_record_kernel<S><<<8, 256, 0, st>>>(reinterpret_cast<const V*>(corners), count, cap, x_offset,
+                                            reinterpret_cast<double2*>(rec));
+}
+
+// G gathered records -> segment g at out[g * cap] (the merge_segments layout)
+// and its count; when at most 64 corners arrived in total, one warp hulls them
+// right here (iterated pruning, warp_hull_small) and raises *done so the
+// following finalize returns at once.
+__global__ void gather_records_kernel(const double2* recs, long long G, long long cap, double2* out, int* seg_cnt,
+                                      int* out_count, int* done) {
+  __shared__ double2 pts[64];
+  __shared__ int total_s;
+  const int tid = threadIdx.x;
+  if (tid == 0) total_s = 0;
+  __syncthreads();
+  for (long long g = 0; g < G; ++g) {
+    const double2* r = recs + g * (cap + 1);
+    const int c = (int)r[0].x;
+    const int k = c < cap ? c : (int)cap;
+    if (tid == 0) seg_cnt[g] = k;
+    const int base = total_s;
+    for (int e = tid; e < k; e += blockDim.x) {
+      const double2 v = r[1 + e];
+      out[g * cap + e] = v;
+      if (base + e < 64) pts[base + e] = v;
+    }
+    __syncthreads();
+    if (tid == 0) total_s = base + k;
+    __syncthreads();
+  }
+  const int total = total_s;
+  if (total <= 64) {
+    if (tid < 32) {
+      const int h = total ? warp_hull_small<double2>(pts, total, pts) : 0;
+      // warp_hull_small wrote the hull in place (dst == P is allowed after its
+      // rounds): copy it out
+      for (int e = tid; e < h; e += 32) out[e] = pts[e];
+      if (tid == 0) {
+        *out_count = h;
+        *done = 1;
+      }
+    }
+  } else if (tid == 0) {
+    *done = 0;
+  }
+}
+
+void launch_gather_records(const double* recs, long long G, long long cap, double* out, int* seg_cnt,
+                           int* out_count, int* done, cudaStream_t st) {
+  gather_records_kernel<<<1, 256, 0, st>>>(reinterpret_cast<const double2*>(recs), G, cap,
+                                            reinterpret_cast<double2*>(out), seg_cnt, out_count, done);
+}
+
 // ------------------------------------------------------------------ host side
 
 // Ring kernel shape: D blocks of lookahead, P blocks in flight per warp, U
@@ -2021,6 +2095,8 @@ template void launch_slab_kernel<float>(const SlabParams<float>&, const CUtensor
 template void launch_slab_kernel<double>(const SlabParams<double>&, const CUtensorMap*, int, cudaStream_t);
 template void launch_finalize<float>(const FinalizeParams<float>&, int, cudaStream_t, bool);
 template void launch_finalize<double>(const FinalizeParams<double>&, int, cudaStream_t, bool);
+template void launch_pack_record<float>(const void*, const int*, long long, double, double*, cudaStream_t);
+template void launch_pack_record<double>(const void*, const int*, long long, double, double*, cudaStream_t);
 template void launch_block_count<float>(const void*, long long, long long, int*, cudaStream_t);
 template void launch_block_count<double>(const void*, long long, long long, int*, cudaStream_t);
 template void launch_pad_fill<float>(void*, const void*, const int*, long long, long long, cudaStream_t);

@@ -47,7 +47,6 @@ struct SlabParams {
   int dbg;                  // 0 normal; 1 stream only (profiling); 2 no merger work
   long long* trace;         // optional per-tile clock64 trace (profiling)
   long long read_lim;       // points at or past this index may not be read yet (host-path chunks)
-  unsigned* pub;            // per unit: order-preserving key of its running max y (zeroed per build)
 };
 
 template <class S>
@@ -62,6 +61,7 @@ struct FinalizeParams {
   long long L;
   int fcap;                 // smem corner capacity of the fast path
   long long* trace;         // optional phase clock64 stamps (profiling)
+  const int* done;          // optional: nonzero = the result is already written (skip)
 };
 
 template <class S>
@@ -73,6 +73,14 @@ void launch_pad_fill(void* padded, const void* corners, const int* counts, long 
                      cudaStream_t st);
 template <class S>
 void launch_block_count(const void* slots, long long n, long long d, int* counts, cudaStream_t st);
+// Multi-GPU exchange records: [count, 0 | corners (double, x + x_offset)], cap corners each.
+template <class S>
+void launch_pack_record(const void* corners, const int* count, long long cap, double x_offset, double* rec,
+                        cudaStream_t st);
+// G records -> segments of stride cap in out (double2) + seg counts; hulls them directly
+// (done = 1) when at most 64 corners arrived in total.
+void launch_gather_records(const double* recs, long long G, long long cap, double* out, int* seg_cnt,
+                           int* out_count, int* done, cudaStream_t st);
 template <class S>
 int slab_kernel_occupancy();    // slab-kernel CTAs per SM
 template <class S>

@@ -64,6 +64,23 @@ def _gather(t, group=None):
     return torch.stack(out)
 
 
+def sharded_build_device(points, corners, counts, rec, gathered, out, out_count, x_offset: float = 0.0,
+                         group=None, block_len: int = 0):
+    """The graph-capturable form used by bench.py: build this rank's slab hood
+    into (corners, counts), pack it (hood_pack_record), all-gather the records
+    over NCCL and merge them (hood_merge_records) -- no host synchronisation.
+    rec (cap+1, 2), gathered (G, cap+1, 2), out (G*cap, 2) float64 buffers."""
+    import torch.distributed as dist
+
+    from . import hood as H
+
+    H.build_hood_async(points, block_len, corners=corners, counts=counts)
+    H.pack_record(corners, counts, rec.shape[0] - 1, x_offset=x_offset, rec=rec)
+    dist.all_gather_into_tensor(gathered.view(-1), rec.view(-1), group=group)
+    H.merge_records(gathered, out=out, out_count=out_count)
+    return out, out_count
+
+
 def merge_gpu(seg_pts, seg_counts):
     """hood_merge_segments over (G, stride, 2) float64 slab hoods."""
     import torch

@@ -41,6 +41,7 @@ EXPORTS = [
     "hood_last_error", "hood_last_launch_count", "hood_status_string", "hood_abi_version",
     "hood_set_profile_events", "hood_merge_round_f32", "hood_merge_round_f64",
     "hood_parse_points", "hood_format_points", "hood_validate_points",
+    "hood_pack_record_f32", "hood_pack_record_f64", "hood_merge_records",
 ]
 
 
@@ -87,6 +88,9 @@ def library():
                 getattr(L, nm).argtypes = [p, p, p, i64, i64, p, p, p]
             for nm in ("hood_merge_round_f32", "hood_merge_round_f64"):
                 getattr(L, nm).argtypes = [p, p, i64, i64, p, p]
+            for nm in ("hood_pack_record_f32", "hood_pack_record_f64"):
+                getattr(L, nm).argtypes = [p, p, p, i64, ctypes.c_double, p, p]
+            L.hood_merge_records.argtypes = [p, p, i64, i64, p, p, p]
             L.hood_last_error.argtypes = [p, ctypes.POINTER(_Err)]
             L.hood_last_launch_count.argtypes = [p]
             L.hood_set_profile_events.argtypes = [p, p, p]
@@ -271,6 +275,44 @@ def merge_segments(seg_pts, seg_counts, out=None, out_count=None, stream=None):
     fn = library().hood_merge_segments_f64 if seg_pts.dtype == torch.float64 else library().hood_merge_segments_f32
     rc = fn(ctx.handle, seg_pts.contiguous().data_ptr(), seg_counts.contiguous().data_ptr(), G, stride,
             out.data_ptr(), out_count.data_ptr(), ctypes.c_void_p(stream.cuda_stream))
+    if rc:
+        _raise(rc)
+    return out, out_count
+
+
+def pack_record(corners, count, cap: int, x_offset: float = 0.0, rec=None, stream=None):
+    """Exchange record of a slab hood (hood_pack_record_*): (cap + 1, 2) float64,
+    row 0 = (count, 0), rows 1.. = corners with x + x_offset.  count is a
+    device int32 tensor (no host sync: graph-capturable)."""
+    import torch
+    dev = corners.device.index if corners.device.index is not None else torch.cuda.current_device()
+    ctx = Context.get(dev)
+    if rec is None:
+        rec = torch.zeros(cap + 1, 2, dtype=torch.float64, device=corners.device)
+    if stream is None:
+        stream = torch.cuda.current_stream(corners.device)
+    fn = library().hood_pack_record_f64 if corners.dtype == torch.float64 else library().hood_pack_record_f32
+    rc = fn(ctx.handle, corners.data_ptr(), count.data_ptr(), cap, float(x_offset), rec.data_ptr(),
+            ctypes.c_void_p(stream.cuda_stream))
+    if rc:
+        _raise(rc)
+    return rec
+
+
+def merge_records(recs, out=None, out_count=None, stream=None):
+    """Global hood from G gathered records (G, cap + 1, 2) float64 (hood_merge_records)."""
+    import torch
+    G, cap = recs.shape[0], recs.shape[1] - 1
+    dev = recs.device.index if recs.device.index is not None else torch.cuda.current_device()
+    ctx = Context.get(dev)
+    if out is None:
+        out = torch.empty(G * cap, 2, dtype=torch.float64, device=recs.device)
+    if out_count is None:
+        out_count = torch.empty(1, dtype=torch.int32, device=recs.device)
+    if stream is None:
+        stream = torch.cuda.current_stream(recs.device)
+    rc = library().hood_merge_records(ctx.handle, recs.contiguous().data_ptr(), G, cap, out.data_ptr(),
+                                      out_count.data_ptr(), ctypes.c_void_p(stream.cuda_stream))
     if rc:
         _raise(rc)
     return out, out_count

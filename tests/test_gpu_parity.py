@@ -385,3 +385,27 @@ def test_merge_round_float_storage_and_in_place(oracle_mod):
     got = t.cpu().numpy()
     assert same(got[: len(h)], h)
     assert np.all(got[len(h):, 0] == 10.0) and np.all(got[len(h):, 1] == 0.0)
+
+
+@pytest.mark.parametrize("G", [1, 2, 8])
+@pytest.mark.parametrize("shape", ["uniform", "arc"])
+def test_pack_and_merge_records(oracle_mod, G, shape):
+    """The multi-GPU exchange kernels on one GPU: G slab hoods packed into
+    records (x shifted by the slab index, exact in double), stacked as the
+    all-gather would, merged -- small totals take the one-warp hull in the
+    gather kernel, large ones (arc) the finalize kernel."""
+    cap = 4096
+    recs, full = [], []
+    for g in range(G):
+        p = (W.grid_uniform(1 << 14, seed=40 + g) if shape == "uniform" else W.arc(1 << 10)).astype(np.float64)
+        t = torch.as_tensor(p.astype(np.float32) if shape == "uniform" else p).cuda()
+        rep = H.build_hood(t)
+        recs.append(H.pack_record(rep.corners, rep.counts, cap, x_offset=float(g)))
+        q = p.copy()
+        q[:, 0] += g
+        full.append(q)
+    out, cnt = H.merge_records(torch.stack(recs))
+    torch.cuda.synchronize()
+    got = out[: int(cnt[0])].cpu().numpy()
+    want = oracle_mod.upper_hull(np.concatenate(full))
+    assert same(got, want), (G, shape)

@@ -37,14 +37,16 @@ for lg in sys.argv[1:] or ["12", "16", "20", "22", "24"]:
         for e in (a, b):
             e.record()
         L.hood_internal_set_debug(ctx.handle, 0, trace.data_ptr())
-        ctx.set_profile_events(a, b)
+        if not os.environ.get("NOEV"):
+            ctx.set_profile_events(a, b)
         H.build_hood_async(pts, block, corners=corners, counts=counts)
         ctx.set_profile_events(None, None)
         L.hood_internal_set_debug(ctx.handle, 0, None)
         torch.cuda.synchronize()
         t = trace[:64].cpu().tolist()
+        fin0 = int(trace[7 * 64 + 30])
     print(f"log2n={lg}: event {a.elapsed_time(b)*1e3:7.1f} us; in-kernel: prologue done +{(t[2]-t[0])/1e3:6.1f} us, "
-          f"last exit +{(t[1]-t[0])/1e3:6.1f} us")
+          f"last exit +{(t[1]-t[0])/1e3:6.1f} us" + (f", finalize starts +{(fin0 - t[0])/1e3:6.1f} us" if fin0 else ""))
     w = trace[1024:1024 + 4 * 8192].view(-1, 4).cpu()
     cyc = trace[1024 + 4 * 8192:].view(-1, 4).cpu()
     keep = w[:, 0] > 0
