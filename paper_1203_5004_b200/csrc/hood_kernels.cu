@@ -39,15 +39,6 @@ __device__ __forceinline__ unsigned char* align1024(unsigned char* p) {
   return p + ((1024u - (a & 1023u)) & 1023u);
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-template <int NT>
-__device__ __forceinline__ void compute_barrier() {
-  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
-}
-
 template <class S>
 __device__ __forceinline__ void load_row(const unsigned char* stage, int t, typename PointT<S>::V* v);
 
@@ -99,15 +90,6 @@ __device__ __forceinline__ S warp_max(S v) {
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
-}
-
-__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
-  return v;
-}
-__device__ __forceinline__ void st_relaxed(unsigned* p, unsigned v) {
-  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 template <class V> __device__ __forceinline__ V make_vec(decltype(V::x) x, decltype(V::x) y) { return V{x, y}; }
@@ -231,165 +213,6 @@ struct HoodState {
   int in_smem;  // 1: Hs in shared memory, 0: spilled to the output slots
 };
 
-// Many survivors in one tile (arc-like input or a slab edge): the merger warp
-// merges the chunk hoods with a warp merge tree, then bridges the tile hood
-// into the running slab hood (kernel.hpp:31-67 classifiers as monotone
-// searches, kernel.cpp:117-137 splice), spilling it to HBM when it outgrows
-// the smem buffer.  Out of line: the common path never touches this code.
-template <class S, int NW, int HC>
-__device__ __noinline__ HoodState merge_tile_tree(unsigned char* tile, const int* nc, const unsigned* wm,
-                                                  long long* mns, int* mnc, typename PointT<S>::V* Hs,
-                                                  typename PointT<S>::V* gslab, HoodState h) {
-  using V = typename PointT<S>::V;
-  constexpr int K = PointT<S>::K;
-  constexpr int NT = NW * 32;
-  const int lane = threadIdx.x & 31;
-  const TileAcc<S> X{tile};
-  for (int c = lane; c < NT; c += 32) {
-    mns[c] = (long long)c * K;
-    mnc[c] = ((wm[c >> 5] >> (c & 31)) & 1u) ? nc[c] : 0;
-  }
-  __syncwarp();
-  int levels = 0;
-  while ((1 << levels) < NT) ++levels;
-  warp_tree_merge<V>(X, mns, mnc, NT, levels, lane);
-  const long long qs = mns[0], kq = mnc[0];
-  long long pidx = -1, qidx = 0;
-  if (lane == 0 && h.n > 0) {
-    if (h.in_smem) bridge<V>(PtrAcc<V>{Hs}, 0, h.n, X, qs, kq, pidx, qidx);
-    else bridge<V>(PtrAcc<V>{gslab}, 0, h.n, X, qs, kq, pidx, qidx);
-  }
-  pidx = __shfl_sync(0xffffffffu, pidx, 0);
-  qidx = __shfl_sync(0xffffffffu, qidx, 0);
-  const long long newN = pidx + 1 + kq - qidx;
-  if (h.in_smem && newN > HC) {  // spill the kept prefix to the output slots
-    for (long long e = lane; e <= pidx; e += 32) gslab[e] = Hs[e];
-    h.in_smem = 0;
-  }
-  V* dstp = h.in_smem ? Hs : gslab;
-  for (long long e = lane; e < kq - qidx; e += 32) dstp[pidx + 1 + e] = X.ld(qs + qidx + e);
-  __syncwarp();
-  h.n = newN;
-  return h;
-}
-
-// Few survivors (the common case): one lane pushes them into the running
-// hood Hs[0..h) in x order, monotone-chain style (oracle.cpp:13-17).
-template <class S, int NW>
-__device__ __noinline__ long long fold_survivors(unsigned char* tile, const int* nc, const unsigned* wm,
-                                                 typename PointT<S>::V* Hs, long long h) {
-  using V = typename PointT<S>::V;
-  constexpr int K = PointT<S>::K;
-  const TileAcc<S> X{tile};
-  V h1 = h >= 1 ? Hs[h - 1] : V{}, h2 = h >= 2 ? Hs[h - 2] : V{};
-  for (int j = 0; j < NW; ++j) {
-    unsigned m = wm[j];
-    while (m) {
-      const int c = 32 * j + __ffs(m) - 1;
-      m &= m - 1;
-      const int cnt = nc[c];
-      for (int e = 0; e < cnt; ++e) {
-        const V q = X.ld((long long)c * K + e);
-        while (h >= 2 && !above(h2, h1, q)) {
-          --h;
-          h1 = h2;
-          if (h >= 2) h2 = Hs[h - 2];
-        }
-        Hs[h] = q;
-        ++h;
-        h2 = h1;
-        h1 = q;
-      }
-    }
-  }
-  return h;
-}
-
-// A partial chunk (only the last chunk of an input): copy its points from
-// global memory into the thread's swizzled row so the hot loop can always
-// read rows from smem.
-template <class S>
-__device__ __noinline__ void stage_partial_row(unsigned char* tile, int t, const typename PointT<S>::V* gpts,
-                                               long long base, int nv) {
-  constexpr int K = PointT<S>::K;
-  const TileAcc<S> X{tile};
-  for (int i = 0; i < K; ++i)
-    X.st((long long)t * K + i, i < nv ? gpts[base + i] : typename PointT<S>::V{});
-}
-
-// Range check of one chunk (validate_points' x in (0,1)), only with
-// HOOD_FLAG_CHECK_RANGE.
-template <class S>
-__device__ __noinline__ void range_check_row(unsigned char* tile, int t, int nv, long long base, DevError* err) {
-  constexpr int K = PointT<S>::K;
-  const TileAcc<S> X{tile};
-  for (int i = 0; i < nv; ++i) {
-    const S x = X.ld((long long)t * K + i).x;
-    if (!(x > (S)0 && x < (S)1)) {
-      atomicMin(&err->key, (unsigned long long)(base + i) * 2);
-      return;
-    }
-  }
-}
-
-// Exact per-chunk anchors inside one warp, for a warp with no anchor on one
-// side (the first / last slab of an instance has nothing beyond it).
-template <class S>
-__device__ __noinline__ S edge_tau(S cm, S left, S right) {
-  const int lane = threadIdx.x & 31;
-  const S NEG = neg_inf<S>();
-  S pin = cm, sin = cm;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const S a = __shfl_up_sync(0xffffffffu, pin, o);
-    const S b = __shfl_down_sync(0xffffffffu, sin, o);
-    if (lane >= o) pin = fmax(pin, a);
-    if (lane + o < 32) sin = fmax(sin, b);
-  }
-  S pex = __shfl_up_sync(0xffffffffu, pin, 1);
-  S sex = __shfl_down_sync(0xffffffffu, sin, 1);
-  if (lane == 0) pex = NEG;
-  if (lane == 31) sex = NEG;
-  return fmin(fmax(left, pex), fmax(right, sex));
-}
-
-template <class S>
-__device__ __forceinline__ S tree_max_y(const typename PointT<S>::V* v) {
-  constexpr int K = PointT<S>::K;
-  S m[K / 2];
-#pragma unroll
-  for (int i = 0; i < K / 2; ++i) m[i] = fmax(v[2 * i].y, v[2 * i + 1].y);
-#pragma unroll
-  for (int w = K / 4; w >= 1; w >>= 1)
-#pragma unroll
-    for (int i = 0; i < w; ++i) m[i] = fmax(m[i], m[i + w]);
-  return m[0];
-}
-
-// Tagged tile maxima: {tile index + 1 (high 32 bits), order-preserving key
-// of the max y (low 32 bits)} in one 64-bit word.  Warps fold their maxima in
-// with a shared-memory atomicMax, so a later tile's tag always wins a slot
-// and a reader can tell a current value from a stale one without any
-// synchronisation.  Doubles are rounded toward -inf first, which keeps the
-// value a valid anchor (never above a real point's y).
-__device__ __forceinline__ unsigned orderable(float f) {
-  const unsigned b = __float_as_uint(f);
-  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-}
-__device__ __forceinline__ float from_orderable(unsigned k) {
-  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
-}
-template <class S>
-__device__ __forceinline__ unsigned long long pack_tagged(long long tile, S m) {
-  const float f = sizeof(S) == 4 ? (float)m : __double2float_rd((double)m);
-  return ((unsigned long long)(unsigned)(tile + 1) << 32) | orderable(f);
-}
-template <class S>
-__device__ __forceinline__ bool tagged_is(unsigned long long w, long long tile, S& val) {
-  val = (S)from_orderable((unsigned)w);
-  return (unsigned)(w >> 32) == (unsigned)(tile + 1);
-}
-
 // ------------------------------------------------------------------ stream kernel
 //
 // The hot kernel.  Every warp is an independent pipeline over its own
@@ -423,21 +246,6 @@ __device__ __forceinline__ float2 pt_of(const float4& q, int e) {
   return e == 0 ? make_float2(q.x, q.y) : make_float2(q.z, q.w);
 }
 __device__ __forceinline__ double2 pt_of(const double2& q, int) { return q; }
-__device__ __forceinline__ float4 ld_stream(const float4* p) { return __ldcs(p); }
-__device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
-
-// Per-warp shared memory of the stream kernel (byte offsets; see WarpLayout).
-template <class S, int U>
-struct StreamLayout {
-  using V = typename PointT<S>::V;
-  static constexpr size_t up(size_t x, size_t a) { return (x + a - 1) / a * a; }
-  static constexpr int BP = 32 * U * Ld16<S>::PPL;                      // points per block
-  static constexpr size_t SB = 0;                                       // [BP] block survivors
-  static constexpr size_t HS = SB + (size_t)BP * sizeof(V);             // [HC] running unit hood
-  static constexpr size_t MNS = up(HS + (size_t)HCap<S>::value * sizeof(V), 8);  // [32] tree starts
-  static constexpr size_t MNC = MNS + 32 * 8;                           // [32] tree counts
-  static constexpr size_t BYTES = up(MNC + 32 * 4, 16);
-};
 
 // Monotone chain over a linear run X[s, s+cnt) in place; returns the corner
 // count (oracle.cpp:7-20).
@@ -583,36 +391,6 @@ __device__ __noinline__ HoodState merge_block_tree(typename PointT<S>::V* SB, in
 // One 16-byte unit of the partial block at the end of an input, reading only
 // the `avail` points that exist; missing points get y = -inf (never survive,
 // never raise an anchor).
-template <class S>
-__device__ __forceinline__ typename Ld16<S>::T partial_load(const typename Ld16<S>::T* src,
-                                                            const typename PointT<S>::V* pt, long long avail);
-template <>
-__device__ __forceinline__ float4 partial_load<float>(const float4* src, const float2* pt, long long avail) {
-  const float NI = neg_inf<float>();
-  if (avail >= 2) return *src;
-  if (avail == 1) {
-    const float2 a = *pt;
-    return make_float4(a.x, a.y, NI, NI);
-  }
-  return make_float4(NI, NI, NI, NI);
-}
-template <>
-__device__ __forceinline__ double2 partial_load<double>(const double2* src, const double2*, long long avail) {
-  const double NI = neg_inf<double>();
-  return avail >= 1 ? *src : make_double2(NI, NI);
-}
-
-template <class S, int U>
-__device__ __forceinline__ S block_ymax(const typename Ld16<S>::T* b) {
-  constexpr int PPL = Ld16<S>::PPL;
-  S m = neg_inf<S>();
-#pragma unroll
-  for (int j = 0; j < U; ++j)
-#pragma unroll
-    for (int e = 0; e < PPL; ++e) m = fmax(m, pt_of(b[j], e).y);
-  return m;
-}
-
 // Slow path of the fused x check: lane-parallel scan of one block for the
 // first point not strictly right of its predecessor (same instance).
 template <class S, int U>
@@ -638,11 +416,6 @@ __device__ __noinline__ void range_check_block(const typename PointT<S>::V* gpts
   }
 }
 
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, int src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)), "l"(gsrc),
-               "r"(src_bytes)
-               : "memory");
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -1432,27 +1205,6 @@ instance_hull_kernel(const __grid_constant__ CUtensorMap tmap, const SlabParams<
 
 // ------------------------------------------------------------------ finalize
 
-// Block-wide exclusive scans over one value per thread (blockDim = 256).
-template <class T, class Op>
-__device__ __forceinline__ T block_excl_scan(T v, T ident, Op op, T* sh, bool reverse) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  T inc = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const T a = reverse ? __shfl_down_sync(0xffffffffu, inc, o) : __shfl_up_sync(0xffffffffu, inc, o);
-    if (reverse ? (lane + o < 32) : (lane >= o)) inc = op(inc, a);
-  }
-  T exc = reverse ? __shfl_down_sync(0xffffffffu, inc, 1) : __shfl_up_sync(0xffffffffu, inc, 1);
-  if (reverse ? lane == 31 : lane == 0) exc = ident;
-  if (reverse ? lane == 0 : lane == 31) sh[warp] = inc;
-  __syncthreads();
-  T carry = ident;
-  for (int w = 0; w < 8; ++w)
-    if (reverse ? (w > warp) : (w < warp)) carry = op(carry, sh[w]);
-  __syncthreads();
-  return op(carry, exc);
-}
-
 // Block-wide exclusive "highest point" scan (blockDim = FT): for every thread,
 // the point of maximal y among the threads before (or after) it.
 template <class V, int NWP>
@@ -1959,7 +1711,7 @@ void launch_gather_records(const double* recs, long long G, long long cap, doubl
 // 16-byte chunks per lane per block (blocks of 2 KB for U = 4, 4 KB for
 // U = 8); selected once per process (HOOD_RING=<D><P><U>, e.g. 234, overrides
 // it for experiments).
-#define HOOD_RING_SHAPES(X) X(2, 3, 4) X(1, 2, 4) X(2, 2, 4) X(1, 1, 8) X(1, 2, 8) X(1, 3, 8) X(2, 2, 8)
+#define HOOD_RING_SHAPES(X) X(1, 1, 8) X(1, 2, 8) X(2, 2, 8) X(2, 3, 4)
 // measured best (B200, round 1): (1, 1, 8) for both storages -- one block of
 // lookahead, one in flight, 4 KB blocks (tools/gpu_sweep.sh)
 template <class S>
