@@ -770,14 +770,18 @@ __global__ void __maxnreg__(HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams
     const long long ibase = (long long)(b / bpi) * p.L;
     const long long lim = min(n, ibase + p.L);
     const long long ub = (long long)b * BP, ue = min((long long)e * BP, lim);
-    const long long l0 = max(ibase, ub - EXT), r1 = min(min(lim, p.read_lim), ue + EXT);
+    // left: EXT points at the start of the previous unit (any input point
+    // left of the unit is a valid anchor, and those are the ones its warp is
+    // streaming right now -- L2 hits, no extra DRAM traffic)
+    const long long ls = max(ibase, ub - (ue - ub));
+    const long long l1 = min(ub, ls + EXT), r1 = min(min(lim, p.read_lim), ue + EXT);
     pl = NEG;
     pr = NEG;
     if (ub > ibase) {
 #pragma unroll
       for (int t = 0; t < EXT / 32; ++t) {  // independent loads: one latency
-        const long long i = ub - EXT + t * 32 + lane;
-        if (i >= l0) pl = fmax(pl, gpts[i].y);
+        const long long i = ls + t * 32 + lane;
+        if (i < l1) pl = fmax(pl, gpts[i].y);
       }
     }
     if (ue < r1) {
