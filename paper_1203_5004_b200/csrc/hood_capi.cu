@@ -476,7 +476,6 @@ int merge_records(hood_ctx* ctx, const double* recs, long long G, long long cap,
   cudaSetDevice(ctx->device);
   int rc;
   if ((rc = ensure_ws(ctx, G))) return rc;
-  cudaMemsetAsync(ctx->err, 0xff, sizeof(DevError), st);
   launch_gather_records(recs, G, cap, out, ctx->seg_cnt, count, ctx->done, st);
   FinalizeParams<double> f{};
   f.out = out;
@@ -489,7 +488,7 @@ int merge_records(hood_ctx* ctx, const double* recs, long long G, long long cap,
   f.L = G * cap;
   f.fcap = (int)(32768 / sizeof(double2));
   f.done = ctx->done;
-  launch_finalize<double>(f, 1, st);
+  launch_finalize<double>(f, 1, st, /*pdl=*/true);  // returns at once when the gather kernel merged
   ctx->last_stream = st;
   ctx->have_last = true;
   ctx->last_launches = 2;

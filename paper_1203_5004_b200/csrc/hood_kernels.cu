@@ -1663,35 +1663,57 @@ void launch_pack_record(const void* corners, const int* count, long long cap, do
 // G gathered records -> segment g at out[g * cap] (the merge_segments layout)
 // and its count; when at most 64 corners arrived in total, one warp hulls them
 // right here (iterated pruning, warp_hull_small) and raises *done so the
-// following finalize returns at once.
-__global__ void gather_records_kernel(const double2* recs, long long G, long long cap, double2* out, int* seg_cnt,
-                                      int* out_count, int* done) {
+// following finalize returns at once.  Headers and corners are read in
+// parallel (one thread per record header).
+__global__ void __launch_bounds__(256) gather_records_kernel(const double2* recs, long long G, long long cap,
+                                                             double2* out, int* seg_cnt, int* out_count, int* done) {
+  asm volatile("griddepcontrol.launch_dependents;");
   __shared__ double2 pts[64];
-  __shared__ int total_s;
+  __shared__ int cnt_s[256], off_s[256 + 1];
   const int tid = threadIdx.x;
-  if (tid == 0) total_s = 0;
+  const bool small = G <= 256;
+  if (small && tid < G) {
+    const int c = (int)recs[(long long)tid * (cap + 1)].x;
+    cnt_s[tid] = c < cap ? c : (int)cap;
+  }
   __syncthreads();
-  for (long long g = 0; g < G; ++g) {
-    const double2* r = recs + g * (cap + 1);
-    const int c = (int)r[0].x;
-    const int k = c < cap ? c : (int)cap;
-    if (tid == 0) seg_cnt[g] = k;
-    const int base = total_s;
-    for (int e = tid; e < k; e += blockDim.x) {
-      const double2 v = r[1 + e];
-      out[g * cap + e] = v;
-      if (base + e < 64) pts[base + e] = v;
+  if (tid == 0) {
+    int o = 0;
+    for (int g = 0; small && g < G; ++g) {
+      off_s[g] = o;
+      o += cnt_s[g];
+    }
+    off_s[small ? G : 0] = small ? o : 65;
+  }
+  __syncthreads();
+  const int total = off_s[small ? G : 0];
+  if (!small) {
+    // many ranks: segments only, the finalize kernel merges
+    for (long long g = tid; g < G; g += blockDim.x) {
+      const int c = (int)recs[g * (cap + 1)].x;
+      seg_cnt[g] = c < cap ? c : (int)cap;
     }
     __syncthreads();
-    if (tid == 0) total_s = base + k;
-    __syncthreads();
+    for (long long g = 0; g < G; ++g) {
+      const int k = seg_cnt[g];
+      for (int e = tid; e < k; e += blockDim.x) out[g * cap + e] = recs[g * (cap + 1) + 1 + e];
+    }
+    if (tid == 0) *done = 0;
+    return;
   }
-  const int total = total_s;
+  for (int g = 0; g < G; ++g) {
+    const int k = cnt_s[g];
+    if (tid == 0) seg_cnt[g] = k;
+    for (int e = tid; e < k; e += blockDim.x) {
+      const double2 v = recs[(long long)g * (cap + 1) + 1 + e];
+      if (total > 64) out[(long long)g * cap + e] = v;
+      else pts[off_s[g] + e] = v;
+    }
+  }
+  __syncthreads();
   if (total <= 64) {
     if (tid < 32) {
       const int h = total ? warp_hull_small<double2>(pts, total, pts) : 0;
-      // warp_hull_small wrote the hull in place (dst == P is allowed after its
-      // rounds): copy it out
       for (int e = tid; e < h; e += 32) out[e] = pts[e];
       if (tid == 0) {
         *out_count = h;
