@@ -409,3 +409,70 @@ def test_pack_and_merge_records(oracle_mod, G, shape):
     got = out[: int(cnt[0])].cpu().numpy()
     want = oracle_mod.upper_hull(np.concatenate(full))
     assert same(got, want), (G, shape)
+
+
+def _shape_points(kind, n, rng):
+    """x strictly increasing on the 2^-24 grid (float-exact); y by shape."""
+    step = max((1 << 24) // n, 1)
+    x = (np.arange(n, dtype=np.int64) * step + rng.integers(1, max(step, 2), size=n)) * 2.0 ** -24
+    x = np.clip(x, 2.0 ** -24, 1 - 2.0 ** -24)
+    x = np.maximum.accumulate(x)
+    x = x + np.arange(n) * 0.0  # keep dtype
+    if kind == "uniform":
+        y = rng.integers(1, 1 << 24, size=n) * 2.0 ** -24
+    elif kind == "sawtooth":
+        y = ((np.arange(n) % 97) / 97.0 * 0.5 + 0.25)
+    elif kind == "steps":
+        y = np.floor(np.arange(n) / max(n // 16, 1)) / 32.0 + 0.1
+    elif kind == "cap":
+        t = x
+        y = 0.2 + t * (1 - t) + rng.integers(0, 8, size=n) * 2.0 ** -24
+    elif kind == "cup":
+        t = x
+        y = 0.8 - t * (1 - t)
+    elif kind == "clusters":
+        y = rng.choice([0.3, 0.5, 0.7], size=n) + rng.integers(0, 1 << 10, size=n) * 2.0 ** -24
+    else:  # "ties": many equal y values
+        y = rng.integers(0, 4, size=n) * 0.125 + 0.25
+    y = np.round(y * 2 ** 24) / 2 ** 24
+    pts = np.stack([x, y], axis=1)
+    keep = np.concatenate([[True], np.diff(pts[:, 0]) > 0])
+    return pts[keep]
+
+
+@pytest.mark.parametrize("kind", ["uniform", "sawtooth", "steps", "cap", "cup", "clusters", "ties"])
+def test_random_shapes_sizes_and_storages(oracle_mod, kind):
+    """Randomised parity sweep: shapes with collinear runs, plateaus and ties,
+    sizes across block/unit boundaries, float2 and double2 storage."""
+    rng = np.random.default_rng(sum(map(ord, kind)))  # stable across processes
+    for n in [3, 31, 512, 513, 4095, 4096, 70001, 1 << 18]:
+        p = _shape_points(kind, n, rng)
+        want = oracle_mod.upper_hull(p)
+        for dt in (torch.float32, torch.float64):
+            got = gpu_hull(p, dtype=dt)
+            assert same(got, want), (kind, n, dt)
+
+
+@pytest.mark.parametrize("L", [512, 1024, 4096, 1 << 14])
+def test_batched_random_shapes(oracle_mod, L):
+    rng = np.random.default_rng(L)
+    inst = max((1 << 18) // L, 2)
+    parts = []
+    for i in range(inst):
+        kind = ["uniform", "cap", "steps", "ties", "sawtooth"][i % 5]
+        q = _shape_points(kind, L, rng)
+        while q.shape[0] < L:  # duplicates removed: pad by re-drawing
+            q = _shape_points(kind, L, rng)
+        parts.append(q[:L])
+    p = np.concatenate(parts)
+    t = torch.as_tensor(p).cuda()
+    rep = H.build_hood(t, block_len=L)
+    c = rep.counts.cpu().numpy()
+    corners = rep.corners.cpu().numpy()
+    for i in range(inst):
+        want = oracle_mod.upper_hull(parts[i])
+        assert same(corners[i * L: i * L + c[i]], want), (L, i)
+    # host path: one strided copy of the widest instance
+    out, counts = H.build_hood_host(np.ascontiguousarray(p), block_len=L)
+    for i in range(inst):
+        assert same(out[i * L: i * L + counts[i]], corners[i * L: i * L + c[i]]), (L, i)
