@@ -476,3 +476,37 @@ def test_batched_random_shapes(oracle_mod, L):
     out, counts = H.build_hood_host(np.ascontiguousarray(p), block_len=L)
     for i in range(inst):
         assert same(out[i * L: i * L + counts[i]], corners[i * L: i * L + c[i]]), (L, i)
+
+
+def test_c_abi_argument_errors():
+    """The C-ABI rejects bad arguments with HOOD_ERR_INVALID_ARG (never a crash
+    or a silent fallback) and keeps working afterwards."""
+    import ctypes
+    L = H.library()
+    ctx = H.Context.get(0)
+    t = torch.as_tensor(W.grid_uniform(1 << 12, seed=3)).cuda()
+    out = torch.empty_like(t)
+    cnt = torch.empty(1, dtype=torch.int32, device="cuda")
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    assert L.hood_build_f32(ctx.handle, t.data_ptr(), 0, 0, out.data_ptr(), cnt.data_ptr(), None, 0, s) == \
+        H.HOOD_ERR_INVALID_ARG                                                      # n = 0
+    assert L.hood_build_f32(ctx.handle, t.data_ptr(), t.shape[0], 3, out.data_ptr(), cnt.data_ptr(), None, 0, s) == \
+        H.HOOD_ERR_INVALID_ARG                                                      # block_len not a power of two
+    assert L.hood_build_f32(ctx.handle, t.data_ptr(), t.shape[0], 1 << 13, out.data_ptr(), cnt.data_ptr(), None,
+                            0, s) == H.HOOD_ERR_INVALID_ARG                         # block_len does not divide n
+    assert L.hood_merge_round_f32(ctx.handle, t.data_ptr(), t.shape[0], 3, out.data_ptr(), s) == \
+        H.HOOD_ERR_INVALID_ARG                                                      # d not a power of two
+    assert L.hood_merge_segments_f64(ctx.handle, None, None, 2, 4, None, None, s) == H.HOOD_ERR_INVALID_ARG
+    assert L.hood_build_f32(None, t.data_ptr(), t.shape[0], 0, out.data_ptr(), cnt.data_ptr(), None, 0, s) != 0
+    # still healthy
+    rep = H.build_hood(t)
+    assert rep.hull.shape[0] >= 2
+
+
+def test_tiny_inputs(oracle_mod):
+    for pts in [[(0.5, 0.5)], [(0.25, 0.1), (0.75, 0.9)], [(0.1, 0.2), (0.2, 0.1), (0.3, 0.2)]]:
+        p = np.array(pts, dtype=np.float64)
+        for dt in (torch.float32, torch.float64):
+            assert same(gpu_hull(p, dtype=dt), oracle_mod.upper_hull(p)), (pts, dt)
+        out, counts = H.build_hood_host(np.ascontiguousarray(p))
+        assert same(out[: counts[0]], oracle_mod.upper_hull(p))
