@@ -71,6 +71,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encoder() {
 
 struct Plan {
   bool hmode = true;
+  bool lean = false;
   long long n = 0, L = 0, instances = 1, tiles = 0, tpi = 0;
   int spi = 1;
   long long units = 0, tpu = 1;
@@ -110,7 +111,11 @@ int make_plan(hood_ctx* ctx, long long n, long long block_len, Plan& pl) {
     pl.spi = (int)spi;
     pl.units = pl.instances * pl.spi;
     if (pl.tpi >= (1LL << 31) || pl.units >= (1LL << 31)) return HOOD_ERR_CAPACITY;
-    pl.grid = (int)std::min((pl.units + nw - 1) / nw, ctas);
+    // batched builds (every unit a whole instance, more instances than warps)
+    // run the register-light ring variant at higher occupancy
+    pl.lean = pl.spi == 1 && pl.instances > 1 && ring_lean_available<S>();
+    const long long ctas_run = pl.lean ? (long long)slab_kernel_occupancy<S>(true) * ctx->sms : ctas;
+    pl.grid = (int)std::min((pl.units + nw - 1) / nw, ctas_run);
   } else {
     const long long resident = (long long)instance_kernel_occupancy<S>() * ctx->sms;
     pl.seg_chunks = (int)(pl.L / K);
@@ -168,6 +173,7 @@ SlabParams<S> slab_params(hood_ctx* ctx, const Plan& pl, const void* pts, void* 
   p.log2L = 0;
   while ((1LL << p.log2L) < pl.L) ++p.log2L;
   p.hmode = pl.hmode ? 1 : 0;
+  p.lean = pl.lean ? 1 : 0;
   p.seg_chunks = pl.seg_chunks;
   p.tiles_per_inst = pl.tpi;
   p.slabs_per_inst = pl.spi;

@@ -291,6 +291,49 @@ __device__ __forceinline__ long long fold_linear(const V* SB, int m, V* Hs, long
   return h;
 }
 
+// Register-light alternative to merge_block_tree (HOOD_RING_LEAN): the same
+// concave fast path, else one lane's monotone-chain pushes into the smem hood
+// or, past its capacity, into the unit's output slots.
+template <class S, int HC>
+__device__ __noinline__ HoodState merge_block_lean(typename PointT<S>::V* SB, int m, typename PointT<S>::V* Hs,
+                                                   typename PointT<S>::V* gslab, HoodState h) {
+  using V = typename PointT<S>::V;
+  const int lane = threadIdx.x & 31;
+  {
+    bool conc = true;
+    for (int i = 1 + lane; i + 1 < m; i += 32) conc = conc && above(SB[i - 1], SB[i], SB[i + 1]);
+    if (__all_sync(0xffffffffu, conc)) {
+      bool join = true;
+      if (lane == 0 && m >= 2) {
+        const V* hsrc = h.in_smem ? Hs : gslab;
+        if (h.n >= 2) join = above(hsrc[h.n - 2], hsrc[h.n - 1], SB[0]);
+        if (join && h.n >= 1) join = above(hsrc[h.n - 1], SB[0], SB[1]);
+      }
+      if (m >= 2 && __shfl_sync(0xffffffffu, join, 0)) {
+        if (h.in_smem && h.n + m > HC) {
+          for (long long i = lane; i < h.n; i += 32) gslab[i] = Hs[i];
+          h.in_smem = 0;
+        }
+        V* dstp = h.in_smem ? Hs : gslab;
+        for (int i = lane; i < m; i += 32) dstp[h.n + i] = SB[i];
+        __syncwarp();
+        h.n += m;
+        return h;
+      }
+    }
+  }
+  if (h.in_smem && h.n + m > HC) {
+    for (long long i = lane; i < h.n; i += 32) gslab[i] = Hs[i];
+    h.in_smem = 0;
+    __syncwarp();
+  }
+  long long nn = h.n;
+  if (lane == 0) nn = fold_linear(SB, m, h.in_smem ? Hs : gslab, nn);
+  h.n = __shfl_sync(0xffffffffu, nn, 0);
+  __syncwarp();
+  return h;
+}
+
 // Strict upper hull of m <= 64 x-sorted points P[0..m) by the whole warp
 // (iterated pruning: a point not strictly above the chord of its alive
 // neighbours lies below the hull and is dropped, geom.hpp:22-28 predicate in
@@ -595,8 +638,10 @@ __device__ __forceinline__ int ring_rot(int l) {
 //   tree + bridge, kernel.hpp:31-67, when many).  A block at an instance edge
 //   (no anchor on one side) gets exact per-point anchors from warp max-scans.
 // Every warp touches only its own smem, so no CTA barrier is ever needed.
-template <class S, int D, int P, int U_>
-__global__ void __maxnreg__(HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams<S> p) {
+// LEAN: batched builds (units = whole instances, never a huge hood per unit)
+// use the register-light merge, 128 registers and 4 CTAs/SM.
+template <class S, int D, int P, int U_, bool LEAN = false>
+__global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams<S> p) {
   using V = typename PointT<S>::V;
   using L = typename Ld16<S>::T;
   using LY = RingLayout<S, D, P, U_>;
@@ -863,7 +908,8 @@ __global__ void __maxnreg__(HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams
       if (lane == 0) h = fold_linear<V>(PBf, pend, Hs, h);
       hs.n = __shfl_sync(FULL, h, 0);
     } else {
-      hs = merge_block_tree<S, HC>(PBf, pend, mns, mnc, Hs, gout + ubase, hs);
+      if constexpr (LEAN) hs = merge_block_lean<S, HC>(PBf, pend, Hs, gout + ubase, hs);
+      else hs = merge_block_tree<S, HC>(PBf, pend, mns, mnc, Hs, gout + ubase, hs);
     }
     pend = 0;
     __syncwarp();
@@ -975,7 +1021,8 @@ __global__ void __maxnreg__(HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams
         if ((svm >> i) & 1u) dst[pos++] = pt_of(c[i / PPL], i % PPL);
       if (total > PC) {
         __syncwarp();
-        hs = merge_block_tree<S, HC>(dst, total, mns, mnc, Hs, gout + ubase, hs);
+        if constexpr (LEAN) hs = merge_block_lean<S, HC>(dst, total, Hs, gout + ubase, hs);
+        else hs = merge_block_tree<S, HC>(dst, total, mns, mnc, Hs, gout + ubase, hs);
         __syncwarp();
       } else {
         pend += total;
@@ -1760,13 +1807,19 @@ static size_t ring_smem() {
   return (size_t)4 * RingLayout<S, D, P, U>::BYTES + 128;  // + alignment pad
 }
 
-template <class S, int D, int P, int U>
+template <class S, int D, int P, int U, bool LEAN = false>
 static int ring_occ_of() {
   const size_t smem = ring_smem<S, D, P, U>();
-  cudaFuncSetAttribute(ring_hull_kernel<S, D, P, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(ring_hull_kernel<S, D, P, U, LEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int o = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ring_hull_kernel<S, D, P, U>, 128, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ring_hull_kernel<S, D, P, U, LEAN>, 128, smem);
   return o > 0 ? o : 1;
+}
+
+// the lean variant exists for the default shape only
+template <class S>
+bool ring_lean_available() {
+  return ring_shape<S>() == kRingDefault<S>;
 }
 
 template <class S>
@@ -1781,7 +1834,13 @@ int slab_warps_per_cta() {
 }
 
 template <class S>
-int slab_kernel_occupancy() {
+int slab_kernel_occupancy(bool lean) {
+  if (lean) {
+    static int occ_lean = -1;
+    if (occ_lean < 0) occ_lean = ring_occ_of<S, kRingDefault<S> / 100, (kRingDefault<S> / 10) % 10, kRingDefault<S> % 10,
+                                             true>();
+    return occ_lean;
+  }
   static int occ = -1;
   if (occ < 0) {
     switch (ring_shape<S>()) {
@@ -1814,7 +1873,12 @@ void launch_slab_kernel(const SlabParams<S>& p, const CUtensorMap* tmap, int gri
     instance_hull_kernel<S><<<grid, kThreads, inst_smem_bytes<S>(), st>>>(*tmap, p);
     return;
   }
-  slab_kernel_occupancy<S>();
+  slab_kernel_occupancy<S>(p.lean != 0);
+  if (p.lean) {
+    constexpr int D = kRingDefault<S> / 100, P = (kRingDefault<S> / 10) % 10, U = kRingDefault<S> % 10;
+    ring_hull_kernel<S, D, P, U, true><<<grid, 128, ring_smem<S, D, P, U>(), st>>>(p);
+    return;
+  }
   switch (ring_shape<S>()) {
 #define HOOD_RING_LAUNCH(D, P, U) \
   case D * 100 + P * 10 + U: ring_hull_kernel<S, D, P, U><<<grid, 128, ring_smem<S, D, P, U>(), st>>>(p); break;
@@ -1879,8 +1943,10 @@ template void launch_block_count<float>(const void*, long long, long long, int*,
 template void launch_block_count<double>(const void*, long long, long long, int*, cudaStream_t);
 template void launch_pad_fill<float>(void*, const void*, const int*, long long, long long, cudaStream_t);
 template void launch_pad_fill<double>(void*, const void*, const int*, long long, long long, cudaStream_t);
-template int slab_kernel_occupancy<float>();
-template int slab_kernel_occupancy<double>();
+template int slab_kernel_occupancy<float>(bool);
+template int slab_kernel_occupancy<double>(bool);
+template bool ring_lean_available<float>();
+template bool ring_lean_available<double>();
 template int instance_kernel_occupancy<float>();
 template int instance_kernel_occupancy<double>();
 template int slab_warps_per_cta<float>();

@@ -12,7 +12,10 @@ constexpr int kThreads = 256;       // one 128-byte chunk row per thread
 constexpr int kStages = 3;          // TMA pipeline depth per CTA
 constexpr int kTileBytes = kThreads * 128;
 constexpr int kHCap = 1024;         // running slab hull kept in smem up to this many corners
-constexpr int kMaxSlabsPerInstance = 2048;
+#ifndef HOOD_MAX_SLABS
+#define HOOD_MAX_SLABS 2048
+#endif
+constexpr int kMaxSlabsPerInstance = HOOD_MAX_SLABS;
 constexpr int kMinUnitBlocks = 2;   // ring kernel: blocks per unit at least
 
 // First error of a build, encoded as key = index*2 + (x_not_increasing ? 1 : 0)
@@ -47,6 +50,7 @@ struct SlabParams {
   int dbg;                  // 0 normal; 1 stream only (profiling); 2 no merger work
   long long* trace;         // optional per-tile clock64 trace (profiling)
   long long read_lim;       // points at or past this index may not be read yet (host-path chunks)
+  int lean;                 // ring kernel: the register-light variant (batched builds)
 };
 
 template <class S>
@@ -82,7 +86,9 @@ void launch_pack_record(const void* corners, const int* count, long long cap, do
 void launch_gather_records(const double* recs, long long G, long long cap, double* out, int* seg_cnt,
                            int* out_count, int* done, cudaStream_t st);
 template <class S>
-int slab_kernel_occupancy();    // slab-kernel CTAs per SM
+int slab_kernel_occupancy(bool lean = false);  // ring-kernel CTAs per SM
+template <class S>
+bool ring_lean_available();     // the register-light ring variant (batched builds) can run
 template <class S>
 int instance_kernel_occupancy();  // instance-kernel CTAs per SM
 template <class S>
