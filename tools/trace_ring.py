@@ -24,6 +24,8 @@ for lg in sys.argv[1:] or ["12", "16", "20", "22", "24"]:
         pts, block = W.batched_torch(65536, 1024, seed=5), 1024
     elif lg.startswith("g"):
         pts = W.gauss_torch(1 << int(lg[1:]), seed=4)
+    elif lg.startswith("a"):
+        pts = W.arc_torch(1 << int(lg[1:]))
     else:
         pts = W.grid_uniform_torch(1 << int(lg), seed=2)
     n = pts.shape[0]
