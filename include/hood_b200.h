@@ -111,6 +111,18 @@ int hood_pack_record_f64(hood_ctx* ctx, const double* d_corners, const int32_t* 
 int hood_merge_records(hood_ctx* ctx, const double* d_recs, int64_t G, int64_t cap, double* d_out,
                        int32_t* d_count, void* stream);
 
+/* Single-process multi-GPU build (one context per device; the P2P form of
+ * the exchange): context g builds the hood of slab g (d_slabs[g], n_per[g]
+ * points on its own device, x in slab g's range, slabs left to right, x
+ * shifted by x_offsets[g] when given), packs it, the records go peer-to-peer
+ * to ctxs[0]'s device, which merges them into d_out (G*cap double2, on
+ * ctxs[0]'s device) and d_count.  Synchronous; slab hoods larger than cap
+ * corners are truncated (size cap to the expected hoods). */
+int hood_build_multi_f32(hood_ctx* const* ctxs, int G, const float* const* d_slabs, const int64_t* n_per,
+                         const double* x_offsets, double* d_out, int32_t* d_count, int64_t cap);
+int hood_build_multi_f64(hood_ctx* const* ctxs, int G, const double* const* d_slabs, const int64_t* n_per,
+                         const double* x_offsets, double* d_out, int32_t* d_count, int64_t cap);
+
 /* One round of the reference round loop (driver.cpp:20-43, the per-round
  * operator launch(match_and_merge_kernel), kernel.cpp:155-161): d_in holds n
  * slots in HoodBuffer layout with blocks of d (each block: its hood's corners

@@ -33,6 +33,10 @@ struct hood_ctx {
   long long seg_cap = 0;
   DevError* err = nullptr;
   int* done = nullptr;      // merge_records: result already written by the gather kernel
+  double* rec = nullptr;    // build_multi: this context's exchange record (cap+1 double2)
+  long long rec_cap = 0;
+  double* gathered = nullptr;  // build_multi (first context): G records
+  long long gathered_elems = 0;
   // host-path buffers
   void* d_in = nullptr;
   size_t d_in_bytes = 0;
@@ -501,9 +505,75 @@ int merge_records(hood_ctx* ctx, const double* recs, long long G, long long cap,
   return cudaGetLastError() == cudaSuccess ? HOOD_OK : HOOD_ERR_CUDA;
 }
 
+// Single-process multi-GPU build (SURVEY.md 8(b) hood_build_multi, the P2P
+// variant of 8(e)): every context builds its slab's hood on its own device
+// and packs its record; the records are copied peer-to-peer (NVLink) to the
+// first context's device, which merges them.  Synchronous.
+template <class S>
+int build_multi(hood_ctx* const* ctxs, int G, const S* const* slabs, const int64_t* n_per, const double* x_off,
+                double* d_out, int* d_count, long long cap) {
+  using V = typename PointT<S>::V;
+  if (!ctxs || G < 1 || !slabs || !n_per || !d_out || !d_count || cap < 1) return HOOD_ERR_INVALID_ARG;
+  if (G > kMaxSlabsPerInstance) return HOOD_ERR_INVALID_ARG;
+  hood_ctx* c0 = ctxs[0];
+  int rc;
+  // 1. every slab: build + pack on its own device and stream
+  for (int g = 0; g < G; ++g) {
+    hood_ctx* c = ctxs[g];
+    if (!c || !slabs[g] || n_per[g] < 1) return HOOD_ERR_INVALID_ARG;
+    cudaSetDevice(c->device);
+    if ((rc = ensure_host_bufs<S>(c, n_per[g], 1))) return rc;
+    if (c->rec_cap < cap) {
+      cudaFree(c->rec);
+      c->rec = nullptr;
+      if (cudaMalloc(&c->rec, (size_t)(cap + 1) * 2 * sizeof(double)) != cudaSuccess) return HOOD_ERR_CUDA;
+      c->rec_cap = cap;
+    }
+    S* corners = reinterpret_cast<S*>(c->d_out);
+    if ((rc = build_device<S>(c, slabs[g], n_per[g], 0, corners, c->d_counts, nullptr, 0, c->s_comp))) return rc;
+    launch_pack_record<S>(corners, c->d_counts, cap, x_off ? x_off[g] : 0.0, c->rec, c->s_comp);
+  }
+  // 2. the records to the first device, after each slab's stream
+  cudaSetDevice(c0->device);
+  const long long need = (long long)G * (cap + 1) * 2;
+  if (c0->gathered_elems < need) {
+    cudaFree(c0->gathered);
+    c0->gathered = nullptr;
+    if (cudaMalloc(&c0->gathered, (size_t)need * sizeof(double)) != cudaSuccess) return HOOD_ERR_CUDA;
+    c0->gathered_elems = need;
+  }
+  for (int g = 0; g < G; ++g) {
+    hood_ctx* c = ctxs[g];
+    cudaSetDevice(c->device);
+    cudaEventRecord(c->ev[0], c->s_comp);
+    cudaSetDevice(c0->device);
+    cudaStreamWaitEvent(c0->s_comp, c->ev[0], 0);
+    cudaMemcpyPeerAsync(c0->gathered + (size_t)g * (cap + 1) * 2, c0->device, c->rec, c->device,
+                        (size_t)(cap + 1) * 2 * sizeof(double), c0->s_comp);
+  }
+  // 3. merge on the first device
+  if ((rc = merge_records(c0, c0->gathered, G, cap, d_out, d_count, c0->s_comp))) return rc;
+  if (cudaStreamSynchronize(c0->s_comp) != cudaSuccess) return HOOD_ERR_CUDA;
+  for (int g = 0; g < G; ++g) {  // validation errors of any slab
+    hood_error e;
+    if ((rc = decode_error(ctxs[g], &e))) return rc;
+  }
+  (void)sizeof(V);
+  return HOOD_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+int hood_build_multi_f32(hood_ctx* const* ctxs, int G, const float* const* d_slabs, const int64_t* n_per,
+                         const double* x_offsets, double* d_out, int32_t* d_count, int64_t cap) {
+  return build_multi<float>(ctxs, G, d_slabs, n_per, x_offsets, d_out, d_count, cap);
+}
+int hood_build_multi_f64(hood_ctx* const* ctxs, int G, const double* const* d_slabs, const int64_t* n_per,
+                         const double* x_offsets, double* d_out, int32_t* d_count, int64_t cap) {
+  return build_multi<double>(ctxs, G, d_slabs, n_per, x_offsets, d_out, d_count, cap);
+}
 
 int hood_pack_record_f32(hood_ctx* ctx, const float* d_corners, const int32_t* d_count, int64_t cap,
                          double x_offset, double* d_rec, void* stream) {
@@ -550,6 +620,8 @@ int hood_destroy(hood_ctx* c) {
   cudaFree(c->seg_base);
   cudaFree(c->err);
   cudaFree(c->done);
+  cudaFree(c->rec);
+  cudaFree(c->gathered);
   cudaFree(c->d_in);
   cudaFree(c->d_out);
   cudaFree(c->d_counts);

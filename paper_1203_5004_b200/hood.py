@@ -42,6 +42,7 @@ EXPORTS = [
     "hood_set_profile_events", "hood_merge_round_f32", "hood_merge_round_f64",
     "hood_parse_points", "hood_format_points", "hood_validate_points",
     "hood_pack_record_f32", "hood_pack_record_f64", "hood_merge_records",
+    "hood_build_multi_f32", "hood_build_multi_f64",
 ]
 
 
@@ -91,6 +92,8 @@ def library():
             for nm in ("hood_pack_record_f32", "hood_pack_record_f64"):
                 getattr(L, nm).argtypes = [p, p, p, i64, ctypes.c_double, p, p]
             L.hood_merge_records.argtypes = [p, p, i64, i64, p, p, p]
+            for nm in ("hood_build_multi_f32", "hood_build_multi_f64"):
+                getattr(L, nm).argtypes = [p, ctypes.c_int, p, p, p, p, p, i64]
             L.hood_last_error.argtypes = [p, ctypes.POINTER(_Err)]
             L.hood_last_launch_count.argtypes = [p]
             L.hood_set_profile_events.argtypes = [p, p, p]
@@ -316,6 +319,28 @@ def merge_records(recs, out=None, out_count=None, stream=None):
     if rc:
         _raise(rc)
     return out, out_count
+
+
+def build_multi(slabs, contexts=None, x_offsets=None, cap: int = 4096):
+    """Single-process multi-GPU build (hood_build_multi_*): slab g is a CUDA
+    tensor on its own device (contexts[g] defaults to that device's context);
+    returns the global hood on slabs[0]'s device, float64."""
+    import torch
+    G = len(slabs)
+    ctxs = contexts or [Context.get(t.device.index if t.device.index is not None else 0) for t in slabs]
+    arr_ctx = (ctypes.c_void_p * G)(*[c.handle.value if hasattr(c.handle, "value") else c.handle for c in ctxs])
+    arr_pts = (ctypes.c_void_p * G)(*[t.data_ptr() for t in slabs])
+    arr_n = (ctypes.c_int64 * G)(*[t.shape[0] for t in slabs])
+    offs = (ctypes.c_double * G)(*(x_offsets if x_offsets is not None else [0.0] * G))
+    dev0 = slabs[0].device
+    out = torch.empty(G * cap, 2, dtype=torch.float64, device=dev0)
+    cnt = torch.empty(1, dtype=torch.int32, device=dev0)
+    fn = library().hood_build_multi_f64 if slabs[0].dtype == torch.float64 else library().hood_build_multi_f32
+    torch.cuda.synchronize(dev0)
+    rc = fn(arr_ctx, G, arr_pts, arr_n, offs, out.data_ptr(), cnt.data_ptr(), cap)
+    if rc:
+        _raise(rc)
+    return out[: int(cnt.item())]
 
 
 def merge_round(slots, d: int, out=None, stream=None):

@@ -510,3 +510,25 @@ def test_tiny_inputs(oracle_mod):
             assert same(gpu_hull(p, dtype=dt), oracle_mod.upper_hull(p)), (pts, dt)
         out, counts = H.build_hood_host(np.ascontiguousarray(p))
         assert same(out[: counts[0]], oracle_mod.upper_hull(p))
+
+
+@pytest.mark.parametrize("G", [1, 3])
+def test_build_multi_single_process(oracle_mod, G):
+    """hood_build_multi (one context per device, P2P record copies to the
+    first device): here G contexts share cuda:0 -- the copies are same-device
+    but take the same code path."""
+    slabs, full = [], []
+    for g in range(G):
+        p = W.grid_uniform(1 << 16, seed=70 + g)
+        slabs.append(torch.as_tensor(p).cuda())
+        q = p.astype(np.float64)
+        q[:, 0] += g
+        full.append(q)
+    ctxs = [H.Context(0) for _ in range(G)]
+    got = H.build_multi(slabs, contexts=ctxs, x_offsets=[float(g) for g in range(G)]).cpu().numpy()
+    assert same(got, oracle_mod.upper_hull(np.concatenate(full)))
+    # double storage, no offsets (slabs already in global coordinates)
+    p = W.gauss(1 << 18, seed=9)
+    parts = np.array_split(p, G)
+    got = H.build_multi([torch.as_tensor(np.ascontiguousarray(x)).cuda() for x in parts], contexts=ctxs).cpu().numpy()
+    assert same(got, oracle_mod.upper_hull(p))
