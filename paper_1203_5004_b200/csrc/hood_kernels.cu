@@ -1707,69 +1707,134 @@ void launch_pack_record(const void* corners, const int* count, long long cap, do
                                             reinterpret_cast<double2*>(rec));
 }
 
-// G gathered records -> segment g at out[g * cap] (the merge_segments layout)
-// and its count; when at most 64 corners arrived in total, one warp hulls them
-// right here (iterated pruning, warp_hull_small) and raises *done so the
-// following finalize returns at once.  Headers and corners are read in
-// parallel (one thread per record header).
+// G gathered records -> the global hood, by one CTA when the exchange is
+// small (G <= 256), else laid out as segments (out[g * cap], seg_cnt) for the
+// finalize kernel.  Small path: when at most 64 corners arrived they are all
+// hulled by one warp (iterated pruning, warp_hull_small).  Otherwise every
+// record's highest corner is its anchor; a corner of record g on or below the
+// chord from the highest anchor left of g to the highest right of g cannot be
+// a corner of the union (the finalize argument); the survivors (x order) are
+// hulled by one warp when at most 64 remain.  *done tells the following
+// finalize whether the result is already written.
 __global__ void __launch_bounds__(256) gather_records_kernel(const double2* recs, long long G, long long cap,
                                                              double2* out, int* seg_cnt, int* out_count, int* done) {
   asm volatile("griddepcontrol.launch_dependents;");
-  __shared__ double2 pts[64];
-  __shared__ int cnt_s[256], off_s[256 + 1];
-  const int tid = threadIdx.x;
-  const bool small = G <= 256;
+  constexpr int GM = 256, NWP = 8;
+  __shared__ double2 stage[64];
+  __shared__ double2 apt_s[GM], A_s[GM], C_s[GM];
+  __shared__ int cnt_s[GM], off_s[GM + 1], kc_s[GM], koff_s[GM + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double NEG = neg_inf<double>();
+  const double2 NOPT = make_double2(NEG, NEG);
+  const bool small = G <= GM;
   if (small && tid < G) {
     const int c = (int)recs[(long long)tid * (cap + 1)].x;
     cnt_s[tid] = c < cap ? c : (int)cap;
   }
   __syncthreads();
-  if (tid == 0) {
+  if (small && tid == 0) {
     int o = 0;
-    for (int g = 0; small && g < G; ++g) {
+    for (int g = 0; g < G; ++g) {
       off_s[g] = o;
       o += cnt_s[g];
     }
-    off_s[small ? G : 0] = small ? o : 65;
+    off_s[G] = o;
   }
   __syncthreads();
-  const int total = off_s[small ? G : 0];
-  if (!small) {
-    // many ranks: segments only, the finalize kernel merges
-    for (long long g = tid; g < G; g += blockDim.x) {
-      const int c = (int)recs[g * (cap + 1)].x;
-      seg_cnt[g] = c < cap ? c : (int)cap;
-    }
-    __syncthreads();
-    for (long long g = 0; g < G; ++g) {
-      const int k = seg_cnt[g];
-      for (int e = tid; e < k; e += blockDim.x) out[g * cap + e] = recs[g * (cap + 1) + 1 + e];
-    }
-    if (tid == 0) *done = 0;
-    return;
-  }
-  for (int g = 0; g < G; ++g) {
-    const int k = cnt_s[g];
-    if (tid == 0) seg_cnt[g] = k;
-    for (int e = tid; e < k; e += blockDim.x) {
-      const double2 v = recs[(long long)g * (cap + 1) + 1 + e];
-      if (total > 64) out[(long long)g * cap + e] = v;
-      else pts[off_s[g] + e] = v;
-    }
-  }
-  __syncthreads();
-  if (total <= 64) {
-    if (tid < 32) {
-      const int h = total ? warp_hull_small<double2>(pts, total, pts) : 0;
-      for (int e = tid; e < h; e += 32) out[e] = pts[e];
-      if (tid == 0) {
+  auto finish = [&](int total) {  // warp 0: hull of stage[0..total)
+    if (warp == 0) {
+      const int h = total ? warp_hull_small<double2>(stage, total, stage) : 0;
+      for (int e = lane; e < h; e += 32) out[e] = stage[e];
+      if (lane == 0) {
         *out_count = h;
         *done = 1;
       }
     }
-  } else if (tid == 0) {
-    *done = 0;
+  };
+  if (small && off_s[G] <= 64) {
+    for (int g = 0; g < G; ++g)
+      for (int e = tid; e < cnt_s[g]; e += blockDim.x) stage[off_s[g] + e] = recs[(long long)g * (cap + 1) + 1 + e];
+    __syncthreads();
+    finish(off_s[G]);
+    return;
   }
+  if (small) {
+    // anchors: one warp per record
+    for (int g = warp; g < G; g += NWP) {
+      const double2* r = recs + (long long)g * (cap + 1) + 1;
+      double2 best = NOPT;
+      for (int e = lane; e < cnt_s[g]; e += 32) {
+        const double2 v = r[e];
+        if (v.y > best.y) best = v;
+      }
+      best = warp_argmax_y(best);
+      if (lane == 0) apt_s[g] = best;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double2 pre = NOPT, suf = NOPT;
+      for (int g = 0; g < G; ++g) {
+        A_s[g] = pre;
+        if (apt_s[g].y > pre.y) pre = apt_s[g];
+      }
+      for (int g = (int)G - 1; g >= 0; --g) {
+        C_s[g] = suf;
+        if (apt_s[g].y > suf.y) suf = apt_s[g];
+      }
+    }
+    __syncthreads();
+    auto keep_of = [&](int g, const double2& v) {
+      const double2 A = A_s[g], Cp = C_s[g];
+      return !(A.y > NEG && Cp.y > NEG) || above(A, v, Cp);
+    };
+    for (int g = warp; g < G; g += NWP) {  // survivors per record
+      const double2* r = recs + (long long)g * (cap + 1) + 1;
+      int k = 0;
+      for (int e0 = 0; e0 < cnt_s[g]; e0 += 32) {
+        const int e = e0 + lane;
+        k += __popc(__ballot_sync(0xffffffffu, e < cnt_s[g] && keep_of(g, r[e < cnt_s[g] ? e : 0])));
+      }
+      if (lane == 0) kc_s[g] = k;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int o = 0;
+      for (int g = 0; g < G; ++g) {
+        koff_s[g] = o;
+        o += kc_s[g];
+      }
+      koff_s[G] = o;
+    }
+    __syncthreads();
+    if (koff_s[G] <= 64) {
+      for (int g = warp; g < G; g += NWP) {
+        const double2* r = recs + (long long)g * (cap + 1) + 1;
+        int k = koff_s[g];
+        for (int e0 = 0; e0 < cnt_s[g]; e0 += 32) {
+          const int e = e0 + lane;
+          const double2 v = r[e < cnt_s[g] ? e : 0];
+          const bool kp = e < cnt_s[g] && keep_of(g, v);
+          const unsigned mk = __ballot_sync(0xffffffffu, kp);
+          if (kp) stage[k + __popc(mk & ((1u << lane) - 1u))] = v;
+          k += __popc(mk);
+        }
+      }
+      __syncthreads();
+      finish(koff_s[G]);
+      return;
+    }
+  }
+  // the finalize kernel merges: records as segments of stride cap
+  for (long long g = tid; g < G; g += blockDim.x) {
+    const int c = (int)recs[g * (cap + 1)].x;
+    seg_cnt[g] = c < cap ? c : (int)cap;
+  }
+  __syncthreads();
+  for (long long g = 0; g < G; ++g) {
+    const int k = seg_cnt[g];
+    for (int e = tid; e < k; e += blockDim.x) out[g * cap + e] = recs[g * (cap + 1) + 1 + e];
+  }
+  if (tid == 0) *done = 0;
 }
 
 void launch_gather_records(const double* recs, long long G, long long cap, double* out, int* seg_cnt,

@@ -57,4 +57,28 @@ for k, name in enumerate(["build", "+pack", "+all_gather", "+merge"]):
         if i >= 3:
             ts.append(a.elapsed_time(b) * 1e3)
     print(f"{name:12s} {statistics.median(ts):7.1f} us")
+
+# the merge of an 8-rank exchange, records prepared from 8 slabs on this GPU
+recs8 = []
+for g in range(8):
+    p = W.grid_uniform_torch(1 << 24, seed=10 + g)
+    rep = H.build_hood(p)
+    recs8.append(H.pack_record(rep.corners, rep.counts, CAP, x_offset=float(g)))
+recs8 = torch.stack(recs8)
+out8 = torch.empty(8 * CAP, 2, dtype=torch.float64, device=dev)
+H.merge_records(recs8, out=out8, out_count=fcnt)
+torch.cuda.synchronize()
+g8 = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g8):
+    H.merge_records(recs8, out=out8, out_count=fcnt)
+ts = []
+for i in range(15):
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    g8.replay()
+    b.record()
+    torch.cuda.synchronize()
+    if i >= 3:
+        ts.append(a.elapsed_time(b) * 1e3)
+print(f"merge of 8 records ({int(recs8[:, 0, 0].sum())} corners -> {int(fcnt)}): {statistics.median(ts):.1f} us")
 dist.destroy_process_group()
