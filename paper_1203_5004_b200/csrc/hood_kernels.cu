@@ -1472,12 +1472,27 @@ __global__ void __launch_bounds__(kFinThreads, 1) finalize_kernel(const Finalize
       long long* rns = nsd;  // reuse the tree-node arrays: hull start / size
       int* rnc = ncd;
       if (p.trace && tid == 0) p.trace[4] = clock64();
-      // one monotone chain (oracle.cpp:7-20) straight over the staged runs
-      // (candidate order = x order) in double (the reference predicate
-      // itself; float inputs were widened exactly), stack in smem
+      // the staged runs in x order (candidate order), widened to double
+      // (exact): up to 64 survivors are hulled by one warp with iterated
+      // pruning (a few rounds of parallel predicates, tools/micro/prune.cu);
+      // more go through one monotone chain (oracle.cpp:7-20)
       double2* Hd = reinterpret_cast<double2*>(F);
       int A = 0;
-      if (tid == 0) {
+      const int v0 = tid < C ? cn[tid] : 0;
+      const int o0 = block_excl_sum<NWP>(v0, shI, &A);
+      if (A <= 64) {
+        for (int e = 0; e < v0; ++e) Hd[o0 + e] = stg[tid * CAP + e];
+        __syncthreads();
+        if (warp == 0) {
+          if (p.trace && lane == 0) p.trace[10] = clock64();
+          const int h = A ? warp_hull_small<double2>(Hd, A, Hd) : 0;
+          if (lane == 0) {
+            rns[0] = 0;
+            rnc[0] = h;
+            if (p.trace) p.trace[11] = clock64();
+          }
+        }
+      } else if (tid == 0) {
         if (p.trace) p.trace[10] = clock64();
         int h = 0;
         double2 h1 = make_double2(0, 0), h2 = h1;
@@ -1496,7 +1511,6 @@ __global__ void __launch_bounds__(kFinThreads, 1) finalize_kernel(const Finalize
             h2 = h1;
             h1 = q;
           }
-          A += m;
         }
         rns[0] = 0;
         rnc[0] = h;
