@@ -1282,6 +1282,42 @@ __device__ __forceinline__ V block_excl_argmax(V v, V ident, V* sh, bool reverse
   return exc.y > carry.y ? exc : carry;
 }
 
+// Both exclusive "highest point" scans at once (before / after every thread),
+// sharing one barrier; shV needs 2 * NWP slots.
+template <class V, int NWP>
+__device__ __forceinline__ void block_excl_argmax2(V v, V ident, V* shV, V& pre, V& suf) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  V up = v, dn = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    V a, b;
+    a.x = __shfl_up_sync(0xffffffffu, up.x, o);
+    a.y = __shfl_up_sync(0xffffffffu, up.y, o);
+    b.x = __shfl_down_sync(0xffffffffu, dn.x, o);
+    b.y = __shfl_down_sync(0xffffffffu, dn.y, o);
+    if (lane >= o && a.y > up.y) up = a;
+    if (lane + o < 32 && b.y > dn.y) dn = b;
+  }
+  V eu, ed;
+  eu.x = __shfl_up_sync(0xffffffffu, up.x, 1);
+  eu.y = __shfl_up_sync(0xffffffffu, up.y, 1);
+  ed.x = __shfl_down_sync(0xffffffffu, dn.x, 1);
+  ed.y = __shfl_down_sync(0xffffffffu, dn.y, 1);
+  if (lane == 0) eu = ident;
+  if (lane == 31) ed = ident;
+  if (lane == 31) shV[warp] = up;
+  if (lane == 0) shV[NWP + warp] = dn;
+  __syncthreads();
+  V cu = ident, cd = ident;
+#pragma unroll
+  for (int w = 0; w < NWP; ++w) {
+    if (w < warp && shV[w].y > cu.y) cu = shV[w];
+    if (w > warp && shV[NWP + w].y > cd.y) cd = shV[NWP + w];
+  }
+  pre = eu.y > cu.y ? eu : cu;
+  suf = ed.y > cd.y ? ed : cd;
+}
+
 // Block-wide exclusive prefix sum (blockDim = 32 * NWP).
 template <int NWP>
 __device__ __forceinline__ int block_excl_sum(int v, int* sh, int* total) {
@@ -1342,14 +1378,14 @@ __global__ void __launch_bounds__(kFinThreads, 1) finalize_kernel(const Finalize
   auto up16 = [](size_t x) { return (x + 15) & ~(size_t)15; };
   const size_t o_ncd = (size_t)M * sizeof(long long);
   const size_t o_shV = up16(o_ncd + (size_t)M * sizeof(int));
-  const size_t o_shI = o_shV + NWP * sizeof(V);
+  const size_t o_shI = o_shV + 2 * NWP * sizeof(V);
   const size_t o_cb = up16(o_shI + (NWP + 8) * sizeof(int));
   const size_t o_cc = o_cb + MAXC * sizeof(long long);
   const size_t o_cn = o_cc + MAXC * sizeof(int);
   const size_t o_cA = up16(o_cn + MAXC * sizeof(int));
   long long* nsd = reinterpret_cast<long long*>(smem_raw);          // [M] tree path
   int* ncd = reinterpret_cast<int*>(smem_raw + o_ncd);              // [M]
-  V* shV = reinterpret_cast<V*>(smem_raw + o_shV);                  // [NWP]
+  V* shV = reinterpret_cast<V*>(smem_raw + o_shV);                  // [2 NWP]
   int* shI = reinterpret_cast<int*>(smem_raw + o_shI);              // [NWP + 8]
   long long* cb = reinterpret_cast<long long*>(smem_raw + o_cb);    // [MAXC]
   int* cc = reinterpret_cast<int*>(smem_raw + o_cc);                // [MAXC] corner count
@@ -1393,8 +1429,8 @@ __global__ void __launch_bounds__(kFinThreads, 1) finalize_kernel(const Finalize
   for (int j = 0; j < R; ++j)
     if (ap[j].y > tbest.y) tbest = ap[j];
   if (p.trace && tid == 0) p.trace[1] = clock64();
-  const V pre_t = block_excl_argmax<V, NWP>(tbest, NOPT, shV, false);
-  const V suf_t = block_excl_argmax<V, NWP>(tbest, NOPT, shV, true);
+  V pre_t, suf_t;
+  block_excl_argmax2<V, NWP>(tbest, NOPT, shV, pre_t, suf_t);
 
   V aA[R], aC[R];
   bool cand[R];
@@ -1465,9 +1501,12 @@ __global__ void __launch_bounds__(kFinThreads, 1) finalize_kernel(const Finalize
     }
     __syncthreads();
     if (p.trace && tid == 0) p.trace[3] = clock64();
-    int ovf = 0;
-    for (int c = tid; c < C; c += kFinThreads) ovf |= cn[c] > CAP;
-    ovf = __syncthreads_or(ovf);
+    // staged counts, their offsets and the overflow flag (a run longer than
+    // CAP was truncated) in one block scan: overflows count in bits 20+
+    int sum_all = 0;
+    const int v0 = tid < C ? min(cn[tid], CAP) : 0;
+    const int o0 = block_excl_sum<NWP>(v0 + ((tid < C && cn[tid] > CAP) ? (1 << 20) : 0), shI, &sum_all) & 0xFFFFF;
+    const int ovf = sum_all >> 20;
     if (!ovf) {
       long long* rns = nsd;  // reuse the tree-node arrays: hull start / size
       int* rnc = ncd;
@@ -1477,9 +1516,7 @@ __global__ void __launch_bounds__(kFinThreads, 1) finalize_kernel(const Finalize
       // pruning (a few rounds of parallel predicates, tools/micro/prune.cu);
       // more go through one monotone chain (oracle.cpp:7-20)
       double2* Hd = reinterpret_cast<double2*>(F);
-      int A = 0;
-      const int v0 = tid < C ? cn[tid] : 0;
-      const int o0 = block_excl_sum<NWP>(v0, shI, &A);
+      const int A = sum_all & 0xFFFFF;
       if (A <= 64) {
         for (int e = 0; e < v0; ++e) Hd[o0 + e] = stg[tid * CAP + e];
         __syncthreads();
