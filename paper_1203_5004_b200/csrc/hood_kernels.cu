@@ -1282,6 +1282,19 @@ __device__ __forceinline__ V block_excl_argmax(V v, V ident, V* sh, bool reverse
   return exc.y > carry.y ? exc : carry;
 }
 
+// Global point load the compiler keeps in program order (volatile asm): a
+// batch of them issued before any use overlaps their latencies.
+__device__ __forceinline__ float2 ldg_pt(const float2* p) {
+  float2 v;
+  asm volatile("ld.global.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double2 ldg_pt(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
 // Both exclusive "highest point" scans at once (before / after every thread),
 // sharing one barrier; shV needs 2 * NWP slots.
 template <class V, int NWP>
@@ -1577,8 +1590,8 @@ __global__ void __launch_bounds__(kFinThreads, 1) finalize_kernel(const Finalize
   for (int j = 0; j < R; ++j) {
     const int s = tid * per + j;
     const bool live = j < per && s < M && sc[j] > 0;
-    e0[j] = live ? gout[sb[j]] : NOPT;
-    e1[j] = live ? gout[sb[j] + sc[j] - 1] : NOPT;
+    e0[j] = ldg_pt(gout + (live ? sb[j] : ibase));
+    e1[j] = ldg_pt(gout + (live ? sb[j] + sc[j] - 1 : ibase));
   }
 #pragma unroll
   for (int j = 0; j < R; ++j) {
@@ -1628,6 +1641,20 @@ __global__ void __launch_bounds__(kFinThreads, 1) finalize_kernel(const Finalize
   int ok = 1, tot = 0;
   {
     int mine = 0;
+    // the four points of every seam, loaded up front (clamped addresses
+    // where a slab is too short; those seams fail below anyway)
+    V p2[R], p1[R], q0[R], q1[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int s = tid * per + j;
+      const bool live = j < per && s + 1 < M;
+      const long long ps = live ? nsd[s] : ibase, qs = live ? nsd[s + 1] : ibase;
+      const int m = live ? ncd[s] : 0, k = live ? ncd[s + 1] : 0;
+      p2[j] = ldg_pt(gout + ps + max(m - 2, 0));
+      p1[j] = ldg_pt(gout + ps + max(m - 1, 0));
+      q0[j] = ldg_pt(gout + qs);
+      q1[j] = ldg_pt(gout + qs + (k >= 2 ? 1 : 0));
+    }
 #pragma unroll
     for (int j = 0; j < R; ++j) {
       const int s = tid * per + j;
@@ -1641,10 +1668,8 @@ __global__ void __launch_bounds__(kFinThreads, 1) finalize_kernel(const Finalize
           if (k == 0) {
             ok = 0;
           } else {
-            const V* P = gout + nsd[s];
-            const V* Q = gout + nsd[s + 1];
-            if (m >= 2) ok &= above(P[m - 2], P[m - 1], Q[0]);
-            if (ok && k >= 2) ok &= above(P[m - 1], Q[0], Q[1]);
+            if (m >= 2) ok &= above(p2[j], p1[j], q0[j]);
+            if (ok && k >= 2) ok &= above(p1[j], q0[j], q1[j]);
           }
         }
       }
