@@ -508,6 +508,18 @@ __device__ __forceinline__ S scan_down_max(S v, int lane) {
 __device__ __forceinline__ void cp_async16s(unsigned dst, const void* gsrc, int src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(gsrc), "r"(src_bytes) : "memory");
 }
+// the same with an L2 eviction policy (the streamed input is evict-first, so
+// the slab hoods the finalize reads back stay in L2)
+__device__ __forceinline__ void cp_async16s(unsigned dst, const void* gsrc, int src_bytes, unsigned long long pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(dst), "l"(gsrc),
+               "r"(src_bytes), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ unsigned long long l2_evict_first_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 template <class L>
 __device__ __forceinline__ L lds16(unsigned a);
 template <>
@@ -588,6 +600,9 @@ __device__ __noinline__ unsigned edge_survivors(unsigned a, long long q0, long l
   return svm;
 }
 
+#ifndef HOOD_L2_EVICT_FIRST
+#define HOOD_L2_EVICT_FIRST 1
+#endif
 #ifndef HOOD_RING_MAXNREG
 #define HOOD_RING_MAXNREG 168
 #endif
@@ -712,12 +727,20 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
   };
   // copy global block b into ring slot s; the input's last block is clamped
   // (cp.async zero-fills the rest)
+#if HOOD_L2_EVICT_FIRST
+  const unsigned long long l2pol = l2_evict_first_policy();
+#endif
   auto issue = [&](int b, int s) {
     const long long off = (long long)b * BB;
     const unsigned dst = wr + s * BB;
     if (b < nfull) {
 #pragma unroll
-      for (int j = 0; j < U; ++j) cp_async16s((dst + j * 512) ^ (U == 8 ? (j & 1) << 6 : 0), gbytes + off + j * 512, 16);
+      for (int j = 0; j < U; ++j)
+#if HOOD_L2_EVICT_FIRST
+        cp_async16s((dst + j * 512) ^ (U == 8 ? (j & 1) << 6 : 0), gbytes + off + j * 512, 16, l2pol);
+#else
+        cp_async16s((dst + j * 512) ^ (U == 8 ? (j & 1) << 6 : 0), gbytes + off + j * 512, 16);
+#endif
     } else {
 #pragma unroll
       for (int j = 0; j < U; ++j) {
@@ -1576,6 +1599,7 @@ __global__ void __launch_bounds__(kFinThreads, 1) finalize_kernel(const Finalize
         p.trace[7] = clock64();
         p.trace[8] = A;
         p.trace[9] = C;
+        p.trace[31] = (long long)gtimer();
       }
       return;
     }
