@@ -32,6 +32,7 @@ struct hood_ctx {
   long long* seg_base = nullptr;
   long long seg_cap = 0;
   DevError* err = nullptr;
+  unsigned* arrive = nullptr;  // finished-unit counter (ring kernel -> finalize), zero between builds
   int* done = nullptr;      // merge_records: result already written by the gather kernel
   double* rec = nullptr;    // build_multi: this context's exchange record (cap+1 double2)
   long long rec_cap = 0;
@@ -134,6 +135,9 @@ int ensure_ws(hood_ctx* ctx, long long slabs) {
   if (!ctx->err) {
     if (cudaMalloc(&ctx->err, sizeof(DevError)) != cudaSuccess) return HOOD_ERR_CUDA;
     if (cudaMalloc(&ctx->done, sizeof(int)) != cudaSuccess) return HOOD_ERR_CUDA;
+    if (cudaMemset(ctx->err, 0xff, sizeof(DevError)) != cudaSuccess) return HOOD_ERR_CUDA;
+    if (cudaMalloc(&ctx->arrive, sizeof(unsigned)) != cudaSuccess) return HOOD_ERR_CUDA;
+    if (cudaMemset(ctx->arrive, 0, sizeof(unsigned)) != cudaSuccess) return HOOD_ERR_CUDA;
   }
   if (slabs > ctx->seg_cap) {
     cudaFree(ctx->seg_cnt);
@@ -253,16 +257,31 @@ int build_device(hood_ctx* ctx, const S* pts, long long n, long long block_len, 
   long long full_rows = 0;
   std::memset(&map, 0, sizeof(map));  // the stream kernel (hmode) reads with LDG, no tensor map
   if (!pl.hmode && (rc = encode_map<S>(pts, n, pl.rows, &map, &full_rows))) return rc;
-  if (cudaMemsetAsync(ctx->err, 0xff, sizeof(DevError), st) != cudaSuccess) return HOOD_ERR_CUDA;
-  const SlabParams<S> p = slab_params<S>(ctx, pl, pts, corners, counts, full_rows, flags);
+  // the ring path resets the error record in-stream (launch_slab_kernel),
+  // except under profile events, which bracket the ring kernel alone
+  const bool reset_in_stream = pl.hmode && !ctx->prof_before;
+  if (!reset_in_stream && cudaMemsetAsync(ctx->err, 0xff, sizeof(DevError), st) != cudaSuccess)
+    return HOOD_ERR_CUDA;
+  SlabParams<S> p = slab_params<S>(ctx, pl, pts, corners, counts, full_rows, flags);
+  // single instance, PDL finalize: it starts on the finished-unit count
+#ifndef HOOD_NO_ARRIVE
+  const bool early = pl.hmode && pl.spi > 1 && pl.instances == 1 && !ctx->prof_after;
+#else
+  const bool early = false;
+#endif
+  p.arrive = early ? ctx->arrive : nullptr;
   if (ctx->prof_before) record_event(ctx->prof_before, st);
-  launch_slab_kernel<S>(p, &map, pl.grid, st);
+  launch_slab_kernel<S>(p, &map, pl.grid, st, reset_in_stream);
   debug_check("slab kernel", st);
   if (ctx->prof_after) record_event(ctx->prof_after, st);
-  int launches = 1;
+  int launches = reset_in_stream ? 2 : 1;  // + the error-reset kernel
   if (pl.hmode && pl.spi > 1) {
-    launch_finalize<S>(finalize_params<S>(ctx, pl, corners, counts), (int)pl.instances, st,
-                       /*pdl=*/!ctx->prof_after);
+    FinalizeParams<S> f = finalize_params<S>(ctx, pl, corners, counts);
+    if (early) {
+      f.arrive = ctx->arrive;
+      f.arrive_target = (unsigned)pl.units;
+    }
+    launch_finalize<S>(f, (int)pl.instances, st, /*pdl=*/!ctx->prof_after);
     debug_check("finalize", st);
     ++launches;
   }
@@ -620,6 +639,7 @@ int hood_destroy(hood_ctx* c) {
   cudaFree(c->seg_base);
   cudaFree(c->err);
   cudaFree(c->done);
+  cudaFree(c->arrive);
   cudaFree(c->rec);
   cudaFree(c->gathered);
   cudaFree(c->d_in);

@@ -149,6 +149,16 @@ __device__ __noinline__ void report_bad(const typename PointT<S>::V* gpts, int n
   if (bad != ~0ULL) atomicMin(&err->key, bad);
 }
 
+// The error record's reset, as the first kernel of a ring build: the ring
+// kernel is its programmatic dependent, starts at once and waits for it
+// (griddepcontrol.wait) only on its rare error paths, right before they touch
+// the record.  A memset node in its place costs the step a full node gap.
+__global__ void err_reset_kernel(DevError* err) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  err->key = ~0ULL;
+}
+__device__ __forceinline__ void err_ready() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 template <class S>
 __device__ __forceinline__ void check_chunk(const typename PointT<S>::V* v, int nv, S prevx, bool has_prev,
                                             long long base, int check_range, DevError* err,
@@ -442,6 +452,7 @@ __device__ __noinline__ void report_bad_block(const typename PointT<S>::V* gpts,
   constexpr int BP = 32 * U * Ld16<S>::PPL;
   const int lane = threadIdx.x & 31;
   const long long e = min(lim, bs + BP);
+  err_ready();
   for (long long q = bs + lane; q < e; q += 32)
     if (q > ibase && !(gpts[q].x > gpts[q - 1].x)) atomicMin(&err->key, (unsigned long long)q * 2 + 1);
 }
@@ -453,6 +464,7 @@ __device__ __noinline__ void range_check_block(const typename PointT<S>::V* gpts
   constexpr int BP = 32 * U * Ld16<S>::PPL;
   const int lane = threadIdx.x & 31;
   const long long e = min(lim, bs + BP);
+  err_ready();
   for (long long q = bs + lane; q < e; q += 32) {
     const S x = gpts[q].x;
     if (!(x > (S)0 && x < (S)1)) atomicMin(&err->key, (unsigned long long)q * 2);
@@ -1109,6 +1121,12 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
         }
       }
       __syncwarp();
+      if constexpr (!LEAN) {
+        if (p.arrive && lane == 0) {  // the unit's hood, count and anchor are published
+          __threadfence();  // cumulative: covers the lanes' writes ordered by the __syncwarp
+          atomicAdd(p.arrive, 1u);
+        }
+      }
       fresh = true;
     }
     advance(cc);
@@ -1395,7 +1413,7 @@ constexpr int kFinCandCap = 32;    // corners staged per candidate
 //      strict upper hull.
 // Huge survivor sets (the arc) merge the slab hoods in place in HBM instead.
 template <class S>
-__global__ void __launch_bounds__(kFinThreads, 1) finalize_kernel(const FinalizeParams<S> p) {
+__device__ __forceinline__ void finalize_body(const FinalizeParams<S>& p) {
   using V = typename PointT<S>::V;
   constexpr int NWP = kFinThreads / 32;
   constexpr int R = kMaxSlabsPerInstance / kFinThreads;  // segments per thread (at most)
@@ -1433,7 +1451,22 @@ __global__ void __launch_bounds__(kFinThreads, 1) finalize_kernel(const Finalize
   double2* stg = reinterpret_cast<double2*>(smem_raw + o_stg);      // [MAXC][CAP]
   V* F = reinterpret_cast<V*>(smem_raw + o_stg + (size_t)MAXC * CAP * sizeof(double2));  // [2][fcap]
 
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the slab kernel has completed
+  if (p.arrive) {
+    // every unit published (the ring kernel's warps may still be exiting):
+    // this skips the wait for the ring grid's completion
+    if (tid == 0) {
+      unsigned v;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.arrive) : "memory");
+        if (v >= p.arrive_target) break;
+        __nanosleep(32);
+      }
+    }
+    __syncthreads();
+    if (tid == 0) *p.arrive = 0u;  // for the next build (every unit has counted)
+  } else {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the slab kernel has completed
+  }
   if (p.done && *p.done) return;  // merged already (small exchange)
   if (p.trace && tid == 0) {
     p.trace[0] = clock64();
@@ -1744,6 +1777,14 @@ __global__ void __launch_bounds__(kFinThreads, 1) finalize_kernel(const Finalize
 // ------------------------------------------------------------------ padding
 
 template <class S>
+__global__ void __launch_bounds__(kFinThreads, 1) finalize_kernel(const FinalizeParams<S> p) {
+  finalize_body<S>(p);
+  // a finalize that started on the unit count (p.arrive) completes only after
+  // the ring grid does, so stream order after it covers both kernels
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+template <class S>
 __global__ void pad_fill_kernel(typename PointT<S>::V* padded, const typename PointT<S>::V* corners,
                                 const int* counts, long long n, long long L) {
   using V = typename PointT<S>::V;
@@ -2032,21 +2073,37 @@ int instance_kernel_occupancy() {
 }
 
 template <class S>
-void launch_slab_kernel(const SlabParams<S>& p, const CUtensorMap* tmap, int grid, cudaStream_t st) {
+void launch_slab_kernel(const SlabParams<S>& p, const CUtensorMap* tmap, int grid, cudaStream_t st, bool reset_err) {
   if (!p.hmode) {
     instance_kernel_occupancy<S>();
     instance_hull_kernel<S><<<grid, kThreads, inst_smem_bytes<S>(), st>>>(*tmap, p);
     return;
   }
+  // reset_err: the error record is reset by a one-thread kernel ahead of the
+  // ring kernel, which follows it as a programmatic dependent
+  if (reset_err) err_reset_kernel<<<1, 1, 0, st>>>(p.err);
   slab_kernel_occupancy<S>(p.lean != 0);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(128);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = reset_err ? 1 : 0;
   if (p.lean) {
     constexpr int D = kRingDefault<S> / 100, P = (kRingDefault<S> / 10) % 10, U = kRingDefault<S> % 10;
-    ring_hull_kernel<S, D, P, U, true><<<grid, 128, ring_smem<S, D, P, U>(), st>>>(p);
+    cfg.dynamicSmemBytes = ring_smem<S, D, P, U>();
+    cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, D, P, U, true>, p);
     return;
   }
   switch (ring_shape<S>()) {
-#define HOOD_RING_LAUNCH(D, P, U) \
-  case D * 100 + P * 10 + U: ring_hull_kernel<S, D, P, U><<<grid, 128, ring_smem<S, D, P, U>(), st>>>(p); break;
+#define HOOD_RING_LAUNCH(D, P, U)                        \
+  case D * 100 + P * 10 + U:                             \
+    cfg.dynamicSmemBytes = ring_smem<S, D, P, U>();      \
+    cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, D, P, U>, p); \
+    break;
     HOOD_RING_SHAPES(HOOD_RING_LAUNCH)
 #undef HOOD_RING_LAUNCH
   }
@@ -2098,8 +2155,8 @@ void launch_pad_fill(void* padded, const void* corners, const int* counts, long 
                                                    reinterpret_cast<const V*>(corners), counts, n, L);
 }
 
-template void launch_slab_kernel<float>(const SlabParams<float>&, const CUtensorMap*, int, cudaStream_t);
-template void launch_slab_kernel<double>(const SlabParams<double>&, const CUtensorMap*, int, cudaStream_t);
+template void launch_slab_kernel<float>(const SlabParams<float>&, const CUtensorMap*, int, cudaStream_t, bool);
+template void launch_slab_kernel<double>(const SlabParams<double>&, const CUtensorMap*, int, cudaStream_t, bool);
 template void launch_finalize<float>(const FinalizeParams<float>&, int, cudaStream_t, bool);
 template void launch_finalize<double>(const FinalizeParams<double>&, int, cudaStream_t, bool);
 template void launch_pack_record<float>(const void*, const int*, long long, double, double*, cudaStream_t);

@@ -51,6 +51,7 @@ struct SlabParams {
   long long* trace;         // optional per-tile clock64 trace (profiling)
   long long read_lim;       // points at or past this index may not be read yet (host-path chunks)
   int lean;                 // ring kernel: the register-light variant (batched builds)
+  unsigned* arrive;         // optional: +1 per finished unit (release), read by the finalize
 };
 
 template <class S>
@@ -66,10 +67,18 @@ struct FinalizeParams {
   int fcap;                 // smem corner capacity of the fast path
   long long* trace;         // optional phase clock64 stamps (profiling)
   const int* done;          // optional: nonzero = the result is already written (skip)
+  // optional (single instance, PDL launch): start when *arrive reaches
+  // arrive_target -- the ring kernel counts finished units -- instead of at the
+  // ring grid's completion; the finalize zeroes it for the next build
+  unsigned* arrive;
+  unsigned arrive_target;
 };
 
 template <class S>
-void launch_slab_kernel(const SlabParams<S>& p, const CUtensorMap* tmap, int grid, cudaStream_t st);
+// reset_err (ring path only): reset the error record in a kernel the ring
+// kernel follows programmatically, instead of a memset node
+void launch_slab_kernel(const SlabParams<S>& p, const CUtensorMap* tmap, int grid, cudaStream_t st,
+                        bool reset_err = false);
 template <class S>
 void launch_finalize(const FinalizeParams<S>& p, int instances, cudaStream_t st, bool pdl = false);
 template <class S>

@@ -304,6 +304,40 @@ def test_graph_capture_replay(oracle_mod):
     assert same(corners[: len(h)].cpu().numpy(), h)
 
 
+@pytest.mark.parametrize("n", [1 << 20, 3000])
+def test_error_record_reset_every_replay(n):
+    """The error record is reset inside the build (a kernel the ring kernel
+    follows programmatically): a replay after a bad one reports clean, a bad
+    one after clean replays reports the right index."""
+    x = np.linspace(0.1, 0.9, n)
+    p = np.stack([x, np.sin(9 * x)], axis=1)
+    t = torch.as_tensor(p).cuda()
+    ctx = H.Context.get(0)
+    corners = torch.empty_like(t)
+    counts = torch.empty(1, dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        H.build_hood_async(t, corners=corners, counts=counts)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        H.build_hood_async(t, corners=corners, counts=counts)
+    bad = n // 3
+    for rnd in range(3):
+        t[bad, 0] = t[bad - 1, 0]
+        g.replay()
+        torch.cuda.synchronize()
+        with pytest.raises(H.ValidationError) as ei:
+            ctx.last_error()
+        assert ei.value.index == bad
+        t[bad, 0] = float(x[bad])
+        g.replay()
+        torch.cuda.synchronize()
+        ctx.last_error()  # clean
+        assert int(counts[0]) > 0
+        bad = n - 1 - rnd
+
+
 def test_cpp_dropin_binary():
     """tests/cpp/test_dropin.cpp: include/hood_b200.hpp from C++, the
     reference's Point2 layout, known answers + random sets + errors."""
