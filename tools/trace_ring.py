@@ -85,3 +85,18 @@ for lg in sys.argv[1:] or ["12", "16", "20", "22", "24"]:
         persm[int(w[i, 2])].append(float(ext[i]))
     smx = sorted((max(v), k) for k, v in persm.items())
     print("   per-SM last exit: min", smx[0], "median", smx[len(smx)//2], "max", smx[-3:])
+    # which warps are slow: by warp-in-CTA, by CTA wave (blockIdx // SMs), by SM
+    idx = torch.nonzero(keep).flatten()
+    gw = idx.double()
+    wic = (idx % 4)
+    cta = idx // 4
+    nsm = len(persm)
+    wave = cta // max(nsm, 1)
+    for nm, key in (("warp in CTA", wic), ("CTA wave", wave)):
+        parts = []
+        for k in sorted(set(key.tolist())):
+            m = key == k
+            parts.append(f"{k}: {float(dur[m].mean()):.1f}")
+        print(f"   mean duration by {nm}: " + ", ".join(parts))
+    if os.environ.get("DUMP"):
+        torch.save({"w": w, "dur": dur, "ext": ext, "idx": idx}, os.environ["DUMP"])
