@@ -24,6 +24,7 @@ slab-parallel upper_hull, every host thread) on the same workload.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -398,6 +399,21 @@ def run_ours(args):
     torch.cuda.synchronize()
     if multi:
         dist.barrier()
+    # attainable-read reference: a bare read of the same input bytes (16-byte
+    # evict-first loads, full occupancy; hood_internal_stream_read), same L2
+    # flush, event-timed -- the time a single-launch stream of this size
+    # takes on this box, start-up and tail included
+    stream_ms = []
+    if not args.no_kernel_events:
+        for i in range(args.steps):
+            flush_l2()
+            kb.record(stream)
+            H.library().hood_internal_stream_read(ctx.handle, ctypes.c_void_p(pts.data_ptr()),
+                                                  ctypes.c_longlong(n * bpp), ctypes.c_void_p(stream.cuda_stream))
+            ka.record(stream)
+            ka.synchronize()
+            stream_ms.append(kb.elapsed_time(ka))
+    torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
     ms = statistics.mean(step_ms)
     kms = statistics.mean(kern_ms)
@@ -442,6 +458,13 @@ def run_ours(args):
     if rank == 0:
         peak, peak_src = peaks()
         achieved = n * bpp / (kms * 1e-3) / 1e9
+        bare_read = None
+        if stream_ms:
+            sms_ = statistics.mean(stream_ms)
+            bare_read = {"ms": sms_, "gbs": n * bpp / (sms_ * 1e-3) / 1e9,
+                         "kernel_vs_bare_read": sms_ / kms,
+                         "what": "one bare read of the same input (evict-first 16 B loads, full occupancy), "
+                                 "same L2 flush: the attainable single-launch read time at this size"}
         cpu = None
         if world == 1:
             hostpts = pts.cpu().numpy()
@@ -466,7 +489,8 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(args.config),
                          "kernel": "ring_hull_kernel", "kernel_ms": kms,
-                         "algorithmic_bytes_per_launch": n * bpp, "peak_source": peak_src},
+                         "algorithmic_bytes_per_launch": n * bpp, "peak_source": peak_src,
+                         "bare_read": bare_read},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

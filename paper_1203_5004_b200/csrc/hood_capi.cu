@@ -713,6 +713,16 @@ extern "C" int hood_internal_set_debug(hood_ctx* ctx, int mode, void* trace) {
   return HOOD_OK;
 }
 
+// Measurement only: one bare read of [p, p + bytes) (bench.py's attainable
+// read time for the same bytes, same flush); async on `stream`.
+extern "C" int hood_internal_stream_read(hood_ctx* ctx, const void* p, long long bytes, void* stream) {
+  if (!ctx || !p || bytes < 16) return HOOD_ERR_INVALID_ARG;
+  cudaSetDevice(ctx->device);
+  if (ensure_ws(ctx, 1)) return HOOD_ERR_CUDA;
+  launch_stream_read(p, bytes, reinterpret_cast<float*>(ctx->done), ctx->sms, reinterpret_cast<cudaStream_t>(stream));
+  return cudaGetLastError() == cudaSuccess ? HOOD_OK : HOOD_ERR_CUDA;
+}
+
 int hood_set_profile_events(hood_ctx* ctx, void* before, void* after) {
   if (!ctx) return HOOD_ERR_INVALID_ARG;
   ctx->prof_before = reinterpret_cast<cudaEvent_t>(before);

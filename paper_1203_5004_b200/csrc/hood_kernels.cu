@@ -919,7 +919,13 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
   for (int i = 0; i + 1 < D; ++i) land_next(i + 1, lmw[i], win[i]);
   lmw[D - 1] = NEG;
   win[D - 1] = NEG;
-  if (p.trace && lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(p.trace) + 2, gtimer());
+  if (p.trace && lane == 0) {
+    const unsigned long long t = gtimer();
+    atomicMax(reinterpret_cast<unsigned long long*>(p.trace) + 2, t);
+#ifndef HOOD_RING_COUNTERS
+    p.trace[1024 + 4 * gw + 3] = (long long)t;  // this warp's prologue end
+#endif
+  }
 
   // per-unit state
   long long u = 0, ubase = 0;
@@ -1782,6 +1788,33 @@ __global__ void __launch_bounds__(kFinThreads, 1) finalize_kernel(const Finalize
   // a finalize that started on the unit count (p.arrive) completes only after
   // the ring grid does, so stream order after it covers both kernels
   asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+// Measurement only (bench.py's attainable-read reference, not on the build
+// path): read `bytes` once with 16-byte evict-first loads, 8 in flight per
+// thread, full occupancy -- the time a bare read of the build's input takes
+// under the same conditions.
+__global__ void __launch_bounds__(256) stream_read_kernel(const float4* __restrict__ in, long long n16,
+                                                          float* sink) {
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  float acc = 0.f;
+  for (; i + 7 * nt < n16; i += 8 * nt) {
+    float4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __ldcs(in + i + k * nt);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc += v[k].x + v[k].y + v[k].z + v[k].w;
+  }
+  for (; i < n16; i += nt) {
+    const float4 v = __ldcs(in + i);
+    acc += v.x + v.y + v.z + v.w;
+  }
+  if (acc == 1.2345e-30f) *sink = acc;  // keeps the loads
+}
+
+void launch_stream_read(const void* p, long long bytes, float* sink, int sms, cudaStream_t st) {
+  stream_read_kernel<<<sms * 8, 256, 0, st>>>(reinterpret_cast<const float4*>(p), bytes / 16, sink);
 }
 
 template <class S>

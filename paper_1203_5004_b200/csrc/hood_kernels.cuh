@@ -79,6 +79,7 @@ template <class S>
 // kernel follows programmatically, instead of a memset node
 void launch_slab_kernel(const SlabParams<S>& p, const CUtensorMap* tmap, int grid, cudaStream_t st,
                         bool reset_err = false);
+void launch_stream_read(const void* p, long long bytes, float* sink, int sms, cudaStream_t st);
 template <class S>
 void launch_finalize(const FinalizeParams<S>& p, int instances, cudaStream_t st, bool pdl = false);
 template <class S>

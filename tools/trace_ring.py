@@ -62,7 +62,11 @@ for lg in sys.argv[1:] or ["12", "16", "20", "22", "24"]:
     q = lambda v: " ".join(f"{float(v.quantile(x)):.1f}" for x in (0, 0.1, 0.5, 0.9, 1.0))
     print(f"   {len(w)} warps; entry q0/10/50/90/100: {q(ent)}; exit: {q(ext)}; duration: {q(dur)}")
     cnt = w[:, 3]
-    if int(cnt.abs().sum()):
+    if int(cnt.min()) > 1 << 40:  # per-warp prologue end (globaltimer) instead of counters
+        pro = (cnt - t[0]).double() / 1e3
+        print(f"   prologue end q0/10/50/90/100: {q(pro)}; exit - prologue end: {q(ext - pro)}")
+        print(f"   corr(prologue end, exit) = {float(torch.corrcoef(torch.stack([pro, ext]))[0, 1]):.2f}")
+    elif int(cnt.abs().sum()):
         cand = (cnt >> 32).double(); edge = ((cnt >> 16) & 0xffff).double(); many = (cnt & 0xffff).double()
         order = torch.argsort(dur)
         print("   fastest (sm, us, cand, edge, many):", [(int(w[i, 2]), round(float(dur[i]), 1), int(cand[i]), int(edge[i]), int(many[i])) for i in order[:8]])
