@@ -572,10 +572,18 @@ __device__ __noinline__ unsigned edge_survivors(unsigned a, long long q0, long l
   for (int k = 0; k < U; ++k) c[k] = lds16<L>(a ^ (k << 4));
   S yv[NP];
   S t = NEG;
+  if (q0 + NP <= n) {  // the lane's whole run exists (every block but the input's last)
 #pragma unroll
-  for (int i = 0; i < NP; ++i) {
-    yv[i] = (q0 + i < n) ? pt_of(c[i / PPL], i % PPL).y : NEG;
-    t = fmax(t, yv[i]);
+    for (int i = 0; i < NP; ++i) {
+      yv[i] = pt_of(c[i / PPL], i % PPL).y;
+      t = fmax(t, yv[i]);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      yv[i] = (q0 + i < n) ? pt_of(c[i / PPL], i % PPL).y : NEG;
+      t = fmax(t, yv[i]);
+    }
   }
   S lft[NP];
   if (runmax == NEG) {
@@ -1026,19 +1034,23 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
       if (tau == NEG) HOOD_COUNT(n_edge);
       else HOOD_COUNT(n_many);
       unsigned svm;
-      L c[U];
-      {
-        const unsigned a = run_addr(lane, s_cur);
-        if (tau == NEG) svm = edge_survivors<S, U>(a, bs + lane * NP, n, runmax, right);
+      const unsigned a = run_addr(lane, s_cur);
+      if (tau == NEG) {
+        svm = edge_survivors<S, U>(a, bs + lane * NP, n, runmax, right);
+      } else {
+        L c[U];
 #pragma unroll
         for (int k = 0; k < U; ++k) c[k] = lds16<L>(a ^ (k << 4));
-      }
-      if (tau != NEG) {
         const long long q0 = bs + lane * NP;
         svm = 0;
+        if (q0 + NP <= n) {
 #pragma unroll
-        for (int i = 0; i < NP; ++i)
-          svm |= ((q0 + i < n) && !(pt_of(c[i / PPL], i % PPL).y < tau) ? 1u : 0u) << i;
+          for (int i = 0; i < NP; ++i) svm |= (!(pt_of(c[i / PPL], i % PPL).y < tau) ? 1u : 0u) << i;
+        } else {
+#pragma unroll
+          for (int i = 0; i < NP; ++i)
+            svm |= ((q0 + i < n) && !(pt_of(c[i / PPL], i % PPL).y < tau) ? 1u : 0u) << i;
+        }
       }
       const int cnt = __popc(svm);
       int incl = cnt;
@@ -1049,17 +1061,26 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
       }
       const int total = __shfl_sync(FULL, incl, 31);
       if (pend + total > PC) flush();
+      int pos = incl - cnt;
       V* dst = PBf + pend;
       if (total > PC) {
         // many survivors: compact them into the block's own slot (every lane
-        // holds its run in registers) and merge them as one batch
+        // holds its run in registers first) and merge them as one batch
+        L c[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) c[k] = lds16<L>(a ^ (k << 4));
         __syncwarp();
         dst = reinterpret_cast<V*>(wb + LY::RING + (size_t)s_cur * BB);
-      }
-      int pos = incl - cnt;
 #pragma unroll
-      for (int i = 0; i < NP; ++i)
-        if ((svm >> i) & 1u) dst[pos++] = pt_of(c[i / PPL], i % PPL);
+        for (int i = 0; i < NP; ++i)
+          if ((svm >> i) & 1u) dst[pos++] = pt_of(c[i / PPL], i % PPL);
+      } else {
+        // few: the lane's survivors straight from the slot, one per set bit
+        for (unsigned m = svm; m; m &= m - 1) {
+          const int i = __ffs(m) - 1;
+          dst[pos++] = lds_pt((a ^ ((i / PPL) << 4)) + (i % PPL) * (unsigned)sizeof(V), (V*)nullptr);
+        }
+      }
       if (total > PC) {
         __syncwarp();
         if constexpr (LEAN) hs = merge_block_lean<S, HC>(dst, total, Hs, gout + ubase, hs);
