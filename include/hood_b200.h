@@ -163,6 +163,25 @@ int hood_parse_points(const char* text, int64_t len, double* xy, int64_t cap, in
 int64_t hood_format_points(const double* xy, int64_t n, char* buf, int64_t cap);
 int hood_validate_points(const double* xy, int64_t n, int64_t* ijk);
 
+/* The reference's run output and round trace (cli.cpp:47-52, 108-118):
+ *   hood_format_section      "<label> <n>" then one "%.17g %.17g" line per
+ *                            point (write_section: label "points" / "hood").
+ *   hood_format_trace_round  one round of the trace from a HoodBuffer layout
+ *                            (hoodbuf.hpp:57-79): "d <d>", then per block of d
+ *                            slots its corner count and corners (the slots
+ *                            before the first REMOTE, x > 1).  The trace ends
+ *                            with a "0" line (write_trace_end).
+ * Both return the byte length and write only when cap suffices.
+ *   hood_write_trace_f64     the whole trace of build_hood with an
+ *                            on_round_begin observer (cli.cpp:163-166) into
+ *                            the file at path: the GPU runs the reference's
+ *                            round loop (hood_merge_round per round, from the
+ *                            input as blocks of 2) and every round's buffer is
+ *                            formatted on the host.  n a power of two >= 2. */
+int64_t hood_format_section(const char* label, const double* xy, int64_t n, char* buf, int64_t cap);
+int64_t hood_format_trace_round(const double* slots, int64_t n, int64_t d, char* buf, int64_t cap);
+int hood_write_trace_f64(hood_ctx* ctx, const double* h_pts, int64_t n, const char* path);
+
 const char* hood_status_string(int status);
 int hood_abi_version(void);
 

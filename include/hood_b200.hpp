@@ -242,4 +242,28 @@ std::string format_points(std::span<const P> pts) {
   return s;
 }
 
+// write_section / write_trace_round (cli.cpp:47-52, 108-118).
+template <class P>
+std::string format_section(const std::string& label, std::span<const P> pts) {
+  detail::check_layout<P>();
+  static_assert(std::is_same_v<detail::scalar_t<P>, double>, "format_section takes {double x, y}");
+  const auto* xy = reinterpret_cast<const double*>(pts.data());
+  const std::int64_t len = hood_format_section(label.c_str(), xy, (std::int64_t)pts.size(), nullptr, 0);
+  std::string s((std::size_t)len, '\0');
+  hood_format_section(label.c_str(), xy, (std::int64_t)pts.size(), s.data(), len);
+  return s;
+}
+
+// The trace file of build_hood under the CLI's on_round_begin observer
+// (cli.cpp:163-169), the round loop run on the GPU.
+template <class P>
+void write_trace(const std::string& path, std::span<const P> pts, int device = 0) {
+  detail::check_layout<P>();
+  static_assert(std::is_same_v<detail::scalar_t<P>, double>, "write_trace takes {double x, y}");
+  hood_ctx* ctx = detail::context(device);
+  const int rc = hood_write_trace_f64(ctx, reinterpret_cast<const double*>(pts.data()), (std::int64_t)pts.size(),
+                                      path.c_str());
+  if (rc != HOOD_OK) throw std::runtime_error(std::string("hood_b200: write_trace: ") + hood_status_string(rc));
+}
+
 }  // namespace hood::b200

@@ -14,6 +14,7 @@
 #include <cstdint>
 #include <cstring>
 #include <mutex>
+#include <vector>
 #include <cstdio>
 #include <cstdlib>
 
@@ -612,6 +613,40 @@ int hood_merge_round_f32(hood_ctx* ctx, const float* d_in, int64_t n, int64_t d,
 }
 int hood_merge_round_f64(hood_ctx* ctx, const double* d_in, int64_t n, int64_t d, double* d_out, void* stream) {
   return merge_round<double>(ctx, d_in, n, d, d_out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+// The round trace of build_hood (cli.cpp:163-166 observer + write_trace_round,
+// cli.cpp:108-118): the input is the HoodBuffer at d = 2 (init_hood,
+// hoodbuf.cpp:88-92); each round is formatted, then merged on the GPU.
+int hood_write_trace_f64(hood_ctx* ctx, const double* h_pts, int64_t n, const char* path) {
+  if (!ctx || !h_pts || !path || n < 2 || (n & (n - 1)) != 0) return HOOD_ERR_INVALID_ARG;
+  cudaSetDevice(ctx->device);
+  FILE* f = std::fopen(path, "wb");
+  if (!f) return HOOD_ERR_INVALID_ARG;
+  const size_t bytes = (size_t)n * 2 * sizeof(double);
+  double *d_a = nullptr, *d_b = nullptr;
+  std::vector<double> h((size_t)n * 2);
+  std::vector<char> text;
+  int rc = HOOD_OK;
+  if (cudaMalloc(&d_a, bytes) != cudaSuccess || cudaMalloc(&d_b, bytes) != cudaSuccess ||
+      cudaMemcpy(d_a, h_pts, bytes, cudaMemcpyHostToDevice) != cudaSuccess)
+    rc = HOOD_ERR_CUDA;
+  std::memcpy(h.data(), h_pts, bytes);
+  // driver.cpp:5-17: rounds while d = d1 * d2 < n, d doubling
+  for (long long d = 2; rc == HOOD_OK && d < n; d *= 2) {
+    const int64_t len = hood_format_trace_round(h.data(), n, d, nullptr, 0);
+    text.resize((size_t)len);
+    hood_format_trace_round(h.data(), n, d, text.data(), len);
+    if (std::fwrite(text.data(), 1, text.size(), f) != text.size()) rc = HOOD_ERR_INVALID_ARG;
+    if (rc == HOOD_OK) rc = merge_round<double>(ctx, d_a, n, d, d_b, 0);
+    if (rc == HOOD_OK && cudaMemcpy(h.data(), d_b, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) rc = HOOD_ERR_CUDA;
+    std::swap(d_a, d_b);
+  }
+  if (rc == HOOD_OK && std::fputs("0\n", f) < 0) rc = HOOD_ERR_INVALID_ARG;  // write_trace_end
+  if (std::fclose(f) != 0 && rc == HOOD_OK) rc = HOOD_ERR_INVALID_ARG;
+  cudaFree(d_a);
+  cudaFree(d_b);
+  return rc;
 }
 
 int hood_create(hood_ctx** out, int device) {

@@ -5,6 +5,8 @@
 //                                          '#' comments; strtod/strtoll tokens;
 //                                          count <= 2^26, cli.cpp:17)
 //   hood_format_points    cli.cpp:101-106 (write_point_set, "%.17g" coords)
+//   hood_format_section   cli.cpp:47-52   (write_section of the run output)
+//   hood_format_trace_round cli.cpp:108-118 (write_trace_round)
 //   hood_validate_points  hoodbuf.cpp:30-70 (power of two, x in (0,1) strictly
 //                                          increasing, collinearity margin
 //                                          1e-9 over all triples for n <= 64,
@@ -116,6 +118,36 @@ int64_t hood_format_points(const double* xy, int64_t n, char* buf, int64_t cap) 
   for (int64_t i = 0; i < n; ++i) {
     const int k = std::snprintf(tmp, sizeof tmp, "%.17g %.17g\n", xy[2 * i], xy[2 * i + 1]);
     out.append(tmp, (size_t)k);
+  }
+  if (buf && cap >= (int64_t)out.size()) std::memcpy(buf, out.data(), out.size());
+  return (int64_t)out.size();
+}
+
+int64_t hood_format_section(const char* label, const double* xy, int64_t n, char* buf, int64_t cap) {
+  if (!label || n < 0 || (n > 0 && !xy)) return -1;
+  std::string out = std::string(label) + " " + std::to_string(n) + "\n";
+  char tmp[96];
+  for (int64_t i = 0; i < n; ++i) {
+    const int k = std::snprintf(tmp, sizeof tmp, "%.17g %.17g\n", xy[2 * i], xy[2 * i + 1]);
+    out.append(tmp, (size_t)k);
+  }
+  if (buf && cap >= (int64_t)out.size()) std::memcpy(buf, out.data(), out.size());
+  return (int64_t)out.size();
+}
+
+int64_t hood_format_trace_round(const double* slots, int64_t n, int64_t d, char* buf, int64_t cap) {
+  if (!slots || n < 1 || d < 1 || n % d != 0) return -1;
+  std::string out = "d " + std::to_string(d) + "\n";
+  char tmp[96];
+  for (int64_t b = 0; b < n / d; ++b) {
+    const double* blk = slots + 2 * b * d;
+    int64_t k = 0;
+    while (k < d && !(blk[2 * k] > 1.0)) ++k;  // block_corners: up to the first REMOTE (geom.hpp:18)
+    out += std::to_string(k) + "\n";
+    for (int64_t i = 0; i < k; ++i) {
+      const int m = std::snprintf(tmp, sizeof tmp, "%.17g %.17g\n", blk[2 * i], blk[2 * i + 1]);
+      out.append(tmp, (size_t)m);
+    }
   }
   if (buf && cap >= (int64_t)out.size()) std::memcpy(buf, out.data(), out.size());
   return (int64_t)out.size();

@@ -41,6 +41,7 @@ EXPORTS = [
     "hood_last_error", "hood_last_launch_count", "hood_status_string", "hood_abi_version",
     "hood_set_profile_events", "hood_merge_round_f32", "hood_merge_round_f64",
     "hood_parse_points", "hood_format_points", "hood_validate_points",
+    "hood_format_section", "hood_format_trace_round", "hood_write_trace_f64",
     "hood_pack_record_f32", "hood_pack_record_f64", "hood_merge_records",
     "hood_build_multi_f32", "hood_build_multi_f64",
 ]

@@ -6,6 +6,11 @@ The reference's front end, restated natively in csrc/hood_host.cpp:
     validate_points(points) hoodbuf.cpp:30-70 -> raises ValidationError
     format_points(points)   cli.cpp:101-106 write_point_set ("%.17g")
     write_point_set(path, points)
+    format_section(label, points)      cli.cpp:47-52 (the run output's sections)
+    format_run_output(points, hull)    cli.cpp:147, 183-184 ("points", "hood")
+    format_trace_round(slots, d)       cli.cpp:108-118 write_trace_round
+    write_trace(path, points)          the trace of build_hood (cli.cpp:163-169),
+                                       the round loop run on the GPU
 """
 from __future__ import annotations
 
@@ -36,6 +41,11 @@ def _lib():
         L.hood_format_points.argtypes = [p, i64, p, i64]
         L.hood_format_points.restype = i64
         L.hood_validate_points.argtypes = [p, i64, ctypes.POINTER(i64 * 3)]
+        L.hood_format_section.argtypes = [ctypes.c_char_p, p, i64, p, i64]
+        L.hood_format_section.restype = i64
+        L.hood_format_trace_round.argtypes = [p, i64, i64, p, i64]
+        L.hood_format_trace_round.restype = i64
+        L.hood_write_trace_f64.argtypes = [p, p, i64, ctypes.c_char_p]
         L._io_bound = True
     return L
 
@@ -91,3 +101,44 @@ def format_points(points) -> str:
 def write_point_set(path: str, points) -> None:
     with open(path, "w") as f:
         f.write(format_points(points))
+
+
+def _text(fn, *args) -> str:
+    n = fn(*args, None, 0)
+    if n < 0:
+        raise ValueError("invalid arguments")
+    buf = ctypes.create_string_buffer(int(n))
+    fn(*args, buf, n)
+    return buf.raw[:n].decode()
+
+
+def format_section(label: str, points) -> str:
+    """write_section (cli.cpp:47-52): "<label> <n>" then one line per point."""
+    a = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 2)
+    return _text(_lib().hood_format_section, label.encode(), a.ctypes.data if a.size else None, a.shape[0])
+
+
+def format_run_output(points, hull, conflicts: int = 0) -> str:
+    """The run output grammar (cli.cpp:147, 183-184): the points section, an
+    optional "# conflicts" comment, then the hood section."""
+    out = format_section("points", points)
+    if conflicts:
+        out += f"# conflicts {conflicts}\n"
+    return out + format_section("hood", hull)
+
+
+def format_trace_round(slots, d: int) -> str:
+    """write_trace_round (cli.cpp:108-118) of a HoodBuffer layout (n slots,
+    blocks of d, corners then REMOTE padding)."""
+    a = np.ascontiguousarray(slots, dtype=np.float64).reshape(-1, 2)
+    return _text(_lib().hood_format_trace_round, a.ctypes.data, a.shape[0], int(d))
+
+
+def write_trace(path: str, points, device: int = 0) -> None:
+    """The trace file of build_hood with the CLI's on_round_begin observer
+    (cli.cpp:163-169): every round's HoodBuffer, then "0".  The round loop runs
+    on the GPU (hood_merge_round per round)."""
+    a = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 2)
+    rc = _lib().hood_write_trace_f64(H.Context.get(device).handle, a.ctypes.data, a.shape[0], path.encode())
+    if rc:
+        H._raise(rc)

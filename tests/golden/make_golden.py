@@ -20,6 +20,10 @@ by oracle/Makefile, plus the extern "C" shim oracle/ref_shim.cpp) and records:
                   cli::parse_points (+ validate_points) outcomes, format_coord
                   strings, validate_points codes (cli.cpp:62-106,
                   hoodbuf.cpp:30-70), incl. tests/data/sample8.txt.
+  trace.npz       the reference's own `hull` run (cli::run through
+                  oracle/_ref/hood_ref_run) with a trace file: the run output
+                  (points / hood sections) and the per-round trace
+                  (cli.cpp:108-118, 144-190) for sample8.txt and random sets.
   pairs.npz       make_random_hood_pair(d, 0xC4C5 + t) windows (acceptance.cpp:79)
                   with the reference classify_g / classify_f tables and the
                   merged block of match_and_merge_block (test_kernel.cpp:302-328).
@@ -219,6 +223,39 @@ def io():
                         varr=np.stack(varr), vres=np.array(vres))
 
 
+def trace():
+    import subprocess
+    import tempfile
+    runner = os.path.join(ROOT, "oracle", "_ref", "hood_ref_run")
+    sample = "/root/reference/proj/tests/data/sample8.txt"
+    inputs = []
+    with open(sample, "rb") as f:
+        inputs.append(f.read())
+    for n in (2, 4, 8, 16, 32, 64, 128, 256, 1024):
+        for s in range(2):
+            inputs.append(O.ref_format_points(O.ref_make_random_point_set(n, 4242 + 17 * s + n)))
+    pts, outs, traces = [], [], []
+    with tempfile.TemporaryDirectory() as td:
+        for k, text in enumerate(inputs):
+            src, tr = os.path.join(td, f"p{k}.txt"), os.path.join(td, f"p{k}.trace")
+            with open(src, "wb") as f:
+                f.write(text)
+            r = subprocess.run([runner, src, tr], capture_output=True, check=True)
+            outs.append(r.stdout)
+            with open(tr, "rb") as f:
+                traces.append(f.read())
+            pts.append(O.ref_parse_points(text)[1])
+
+    def blob(items):
+        off = np.cumsum([0] + [len(x) for x in items])
+        return np.frombuffer(b"".join(items), dtype=np.uint8), off
+    ob, oo = blob(outs)
+    tb, to = blob(traces)
+    np.savez_compressed(os.path.join(OUT, "trace.npz"), pts=np.concatenate(pts),
+                        pts_off=np.cumsum([0] + [len(p) for p in pts]), out_blob=ob, out_off=oo,
+                        trace_blob=tb, trace_off=to)
+
+
 if __name__ == "__main__":
     O.build(ref=True)
     acceptance()
@@ -226,6 +263,7 @@ if __name__ == "__main__":
     raw()
     pairs()
     io()
+    trace()
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -566,3 +566,18 @@ def test_build_multi_single_process(oracle_mod, G):
     parts = np.array_split(p, G)
     got = H.build_multi([torch.as_tensor(np.ascontiguousarray(x)).cuda() for x in parts], contexts=ctxs).cpu().numpy()
     assert same(got, oracle_mod.upper_hull(p))
+
+
+def test_trace_file_matches_reference(golden, tmp_path):
+    """write_trace: the reference's round loop on the GPU (hood_merge_round per
+    round) with the CLI's on_round_begin trace writer (cli.cpp:108-118,
+    163-169), byte-identical to the reference's own `hull` run."""
+    from paper_1203_5004_b200 import io as IO
+    g = golden("trace.npz")
+    off, toff = g["pts_off"], g["trace_off"]
+    blob = bytes(g["trace_blob"])
+    for i in range(len(off) - 1):
+        pts = g["pts"][off[i]:off[i + 1]]
+        path = tmp_path / f"t{i}.trace"
+        IO.write_trace(str(path), pts)
+        assert path.read_bytes() == blob[toff[i]:toff[i + 1]], len(pts)
