@@ -1478,6 +1478,7 @@ __device__ __forceinline__ void finalize_body(const FinalizeParams<S>& p) {
   double2* stg = reinterpret_cast<double2*>(smem_raw + o_stg);      // [MAXC][CAP]
   V* F = reinterpret_cast<V*>(smem_raw + o_stg + (size_t)MAXC * CAP * sizeof(double2));  // [2][fcap]
 
+  if (p.trace && threadIdx.x == 0) p.trace[29] = (long long)gtimer();  // resident
   if (p.arrive) {
     // every unit published (the ring kernel's warps may still be exiting):
     // this skips the wait for the ring grid's completion
@@ -1614,7 +1615,13 @@ __device__ __forceinline__ void finalize_body(const FinalizeParams<S>& p) {
       double2* Hd = reinterpret_cast<double2*>(F);
       const int A = sum_all & 0xFFFFF;
       if (A <= 64) {
-        for (int e = 0; e < v0; ++e) Hd[o0 + e] = stg[tid * CAP + e];
+        // the staged runs to their offsets: a warp per run, a lane per corner
+        // (CAP == 32); cc (corner counts) is free after the staging
+        if (tid < C) cc[tid] = o0;
+        __syncthreads();
+        static_assert(CAP == 32, "one lane per staged corner");
+        for (int c = warp; c < C; c += NWP)
+          if (lane < min(cn[c], CAP)) Hd[cc[c] + lane] = stg[c * CAP + lane];
         __syncthreads();
         if (warp == 0) {
           if (p.trace && lane == 0) p.trace[10] = clock64();

@@ -58,9 +58,11 @@ for lg in sys.argv[1:] or ["12", "16", "20", "22", "24"]:
         t = trace[:64].cpu().tolist()
         fin0 = int(trace[7 * 64 + 30])
         fin1 = int(trace[7 * 64 + 31])
+        finr = int(trace[7 * 64 + 29])
     print(f"log2n={lg}: event {a.elapsed_time(b)*1e3:7.1f} us; in-kernel: prologue done +{(t[2]-t[0])/1e3:6.1f} us, "
           f"last exit +{(t[1]-t[0])/1e3:6.1f} us" + (f", finalize starts +{(fin0 - t[0])/1e3:6.1f} us" if fin0 else "")
-          + (f", ends +{(fin1 - t[0])/1e3:6.1f} us" if fin1 else ""))
+          + (f", ends +{(fin1 - t[0])/1e3:6.1f} us" if fin1 else "")
+          + (f"; finalize CTA resident +{(finr - t[0])/1e3:6.1f} us" if finr else ""))
     w = trace[1024:1024 + 4 * 8192].view(-1, 4).cpu()
     cyc = trace[1024 + 4 * 8192:].view(-1, 4).cpu()
     keep = w[:, 0] > 0
