@@ -55,7 +55,10 @@ typedef struct hood_error {
 #define HOOD_FLAG_CHECK_RANGE 0x1u /* also reject x outside (0, 1) (validate_points) */
 
 /* One context per device and host thread (the reference build is reentrant,
- * SPEC.md:423; contexts share nothing). */
+ * SPEC.md:423; contexts share nothing).  A context owns one device workspace
+ * (unit summaries, error record, finished-unit counter): its builds must be
+ * ordered on one stream (or synchronized); concurrent builds take one context
+ * each. */
 int hood_create(hood_ctx** ctx, int device);
 int hood_destroy(hood_ctx* ctx);
 
