@@ -265,11 +265,7 @@ int build_device(hood_ctx* ctx, const S* pts, long long n, long long block_len, 
     return HOOD_ERR_CUDA;
   SlabParams<S> p = slab_params<S>(ctx, pl, pts, corners, counts, full_rows, flags);
   // single instance, PDL finalize: it starts on the finished-unit count
-#ifndef HOOD_NO_ARRIVE
   const bool early = pl.hmode && pl.spi > 1 && pl.instances == 1 && !ctx->prof_after;
-#else
-  const bool early = false;
-#endif
   p.arrive = early ? ctx->arrive : nullptr;
   if (ctx->prof_before) record_event(ctx->prof_before, st);
   launch_slab_kernel<S>(p, &map, pl.grid, st, reset_in_stream);
