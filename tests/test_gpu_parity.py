@@ -581,3 +581,36 @@ def test_trace_file_matches_reference(golden, tmp_path):
         path = tmp_path / f"t{i}.trace"
         IO.write_trace(str(path), pts)
         assert path.read_bytes() == blob[toff[i]:toff[i + 1]], len(pts)
+
+
+def test_finished_unit_counter_across_builds(oracle_mod):
+    """The finalize of a single-instance build starts on a finished-unit
+    counter that it resets for the next build: interleaved sizes (different
+    unit counts), batched builds in between, and graph replays must all see a
+    clean counter and produce the oracle's hood."""
+    ctx = H.Context.get(0)
+    sets = [W.grid_uniform(1 << 20, seed=31), W.gauss(1 << 22, seed=32), W.grid_uniform(1 << 18, seed=33)]
+    ts = [torch.as_tensor(p).cuda() for p in sets]
+    want = [oracle_mod.upper_hull(p) for p in sets]
+    bat = torch.as_tensor(W.batched(256, 1024, seed=34)).cuda()
+    for rnd in range(3):
+        for t, w in zip(ts, want):
+            assert same(H.build_hood(t).hull.cpu().numpy(), w)
+            H.build_hood(bat, block_len=1024)
+    t = ts[0]
+    ctx.reserve(t.shape[0])
+    corners = torch.empty_like(t)
+    counts = torch.empty(1, dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        H.build_hood_async(t, corners=corners, counts=counts)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        H.build_hood_async(t, corners=corners, counts=counts)
+    for rnd in range(5):
+        corners.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert same(corners[: int(counts[0])].cpu().numpy(), want[0])
+        assert same(H.build_hood(ts[1]).hull.cpu().numpy(), want[1])
