@@ -1421,7 +1421,10 @@ __device__ __forceinline__ int block_excl_sum(int v, int* sh, int* total) {
   return carry + inc - v;
 }
 
-constexpr int kFinThreads = 256;
+#ifndef HOOD_FIN_THREADS
+#define HOOD_FIN_THREADS 512
+#endif
+constexpr int kFinThreads = HOOD_FIN_THREADS;
 constexpr int kFinCand = 128;      // candidate slabs handled in smem
 constexpr int kFinCandCap = 32;    // corners staged per candidate
 
