@@ -110,7 +110,8 @@ int make_plan(hood_ctx* ctx, long long n, long long block_len, Plan& pl) {
     pl.seg_chunks = 32;
     pl.tpi = (pl.L + T - 1) / T;
     long long spi = ctas * nw / pl.instances;
-    // units of at least kMinUnitBlocks blocks keep the per-unit overhead
+    // units of at least kMinUnitBlocks blocks (1: small inputs spread over
+    // as many warps as they have blocks) keep the per-unit overhead
     // (edge anchors, hood write-out, finalize candidates) small
     spi = std::min(spi, std::max(1LL, pl.tpi / kMinUnitBlocks));
     spi = std::max(1LL, std::min(spi, std::min(pl.tpi, (long long)kMaxSlabsPerInstance)));

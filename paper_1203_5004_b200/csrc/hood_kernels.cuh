@@ -16,7 +16,10 @@ constexpr int kHCap = 1024;         // running slab hull kept in smem up to this
 #define HOOD_MAX_SLABS 2048
 #endif
 constexpr int kMaxSlabsPerInstance = HOOD_MAX_SLABS;
-constexpr int kMinUnitBlocks = 2;   // ring kernel: blocks per unit at least
+#ifndef HOOD_MIN_UNIT_BLOCKS
+#define HOOD_MIN_UNIT_BLOCKS 1
+#endif
+constexpr int kMinUnitBlocks = HOOD_MIN_UNIT_BLOCKS;  // ring kernel: blocks per unit at least
 
 // First error of a build, encoded as key = index*2 + (x_not_increasing ? 1 : 0)
 // so one atomicMin keeps validate_points' order (hoodbuf.cpp:48-58: at the
