@@ -620,6 +620,10 @@ __device__ __noinline__ unsigned edge_survivors(unsigned a, long long q0, long l
   return svm;
 }
 
+#ifndef HOOD_RING_WARPS
+#define HOOD_RING_WARPS 4
+#endif
+constexpr int kRingWarps = HOOD_RING_WARPS;  // warps (independent pipelines) per ring CTA
 #ifndef HOOD_L2_EVICT_FIRST
 #define HOOD_L2_EVICT_FIRST 1
 #endif
@@ -2074,7 +2078,7 @@ static int ring_shape() {
 
 template <class S, int D, int P, int U>
 static size_t ring_smem() {
-  return (size_t)4 * RingLayout<S, D, P, U>::BYTES + 128;  // + alignment pad
+  return (size_t)kRingWarps * RingLayout<S, D, P, U>::BYTES + 128;  // + alignment pad
 }
 
 template <class S, int D, int P, int U, bool LEAN = false>
@@ -2082,7 +2086,7 @@ static int ring_occ_of() {
   const size_t smem = ring_smem<S, D, P, U>();
   cudaFuncSetAttribute(ring_hull_kernel<S, D, P, U, LEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int o = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ring_hull_kernel<S, D, P, U, LEAN>, 128, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ring_hull_kernel<S, D, P, U, LEAN>, 32 * kRingWarps, smem);
   return o > 0 ? o : 1;
 }
 
@@ -2100,7 +2104,7 @@ int slab_tile_rows(bool hmode) {
 
 template <class S>
 int slab_warps_per_cta() {
-  return 4;
+  return kRingWarps;
 }
 
 template <class S>
@@ -2149,7 +2153,7 @@ void launch_slab_kernel(const SlabParams<S>& p, const CUtensorMap* tmap, int gri
   slab_kernel_occupancy<S>(p.lean != 0);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(128);
+  cfg.blockDim = dim3(32 * kRingWarps);
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
