@@ -1130,15 +1130,23 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
             for (long long e = lane; e < hs.n; e += 32)
               if (Hs[e].y > apt.y) apt = Hs[e];
             apt = warp_argmax_y(apt);
-          } else if (lane == 0) {
+          } else {
+            // spilled (huge) hood in HBM: a 32-way search, one round trip per
+            // 32x narrowing -- the highest of 32 evenly spaced samples brackets
+            // the peak of a unimodal sequence between its two neighbours
             const V* h = gout + ubase;
             long long a = 0, b = hs.n - 1;
-            while (a < b) {
-              const long long mid = (a + b) >> 1;
-              if (h[mid + 1].y > h[mid].y) a = mid + 1;
-              else b = mid;
+            while (b - a >= 32) {
+              const long long pos = a + (b - a) * lane / 31;
+              const V q = h[pos];
+              const int k = __ffs(__ballot_sync(FULL, q.y == warp_max(q.y))) - 1;
+              const long long lo = a + (b - a) * max(k - 1, 0) / 31;
+              const long long hi = a + (b - a) * min(k + 1, 31) / 31;
+              a = lo;
+              b = hi;
             }
-            apt = h[a];
+            const V q = a + lane <= b ? h[a + lane] : make_vec<V>(NEG, NEG);
+            apt = warp_argmax_y(q);
           }
         }
         if (lane == 0) reinterpret_cast<V*>(p.seg_apt)[u] = apt;
