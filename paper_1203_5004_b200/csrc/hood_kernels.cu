@@ -1111,15 +1111,18 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
 
     if (nrem == 0) {
       // unit done: its hood to the output slots, its summary for finalize
+      bool written = false;
       if (hs.in_smem && hs.n == 0 && pend <= PC) {
         // the whole unit's survivors are still queued (short units, batched
-        // instances): hull them with the warp, straight into the output slots
-        hs.n = pend ? warp_hull_small<V>(PBf, pend, Hs) : 0;
+        // instances): hull them with the warp -- straight into the output
+        // slots when no anchor point is needed (whole instances)
+        written = spi == 1;
+        hs.n = pend ? warp_hull_small<V>(PBf, pend, written ? gout + ubase : Hs) : 0;
         pend = 0;
       } else {
         flush();
       }
-      if (hs.in_smem)
+      if (hs.in_smem && !written)
         for (long long e = lane; e < hs.n; e += 32) gout[ubase + e] = Hs[e];
       if (spi > 1) {
         // anchor point for finalize: the unit's highest hood corner (a real
