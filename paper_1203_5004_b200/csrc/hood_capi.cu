@@ -34,6 +34,7 @@ struct hood_ctx {
   long long seg_cap = 0;
   DevError* err = nullptr;
   unsigned* arrive = nullptr;  // finished-unit counter (ring kernel -> finalize), zero between builds
+  void* warm = nullptr;        // the finalize's warm-up instance (kWarmBytes)
   int* done = nullptr;      // merge_records: result already written by the gather kernel
   double* rec = nullptr;    // build_multi: this context's exchange record (cap+1 double2)
   long long rec_cap = 0;
@@ -140,6 +141,10 @@ int ensure_ws(hood_ctx* ctx, long long slabs) {
     if (cudaMemset(ctx->err, 0xff, sizeof(DevError)) != cudaSuccess) return HOOD_ERR_CUDA;
     if (cudaMalloc(&ctx->arrive, sizeof(unsigned)) != cudaSuccess) return HOOD_ERR_CUDA;
     if (cudaMemset(ctx->arrive, 0, sizeof(unsigned)) != cudaSuccess) return HOOD_ERR_CUDA;
+    if (cudaMalloc(&ctx->warm, kWarmBytes) != cudaSuccess) return HOOD_ERR_CUDA;
+    // zero counts until the first reset kernel writes the instance (same
+    // bytes every build, so a finalize never reads a torn one)
+    if (cudaMemset(ctx->warm, 0, kWarmBytes) != cudaSuccess) return HOOD_ERR_CUDA;
   }
   if (slabs > ctx->seg_cap) {
     cudaFree(ctx->seg_cnt);
@@ -269,7 +274,12 @@ int build_device(hood_ctx* ctx, const S* pts, long long n, long long block_len, 
   const bool early = pl.hmode && pl.spi > 1 && pl.instances == 1 && !ctx->prof_after;
   p.arrive = early ? ctx->arrive : nullptr;
   if (ctx->prof_before) record_event(ctx->prof_before, st);
-  launch_slab_kernel<S>(p, &map, pl.grid, st, reset_in_stream);
+  // the finalize's warm-up merge pays only when its CTA is resident early,
+  // i.e. when the ring grid leaves SMs free (small inputs: config 1 -10%);
+  // on a full GPU it would run past the last unit and delay the real merge
+  const bool warm_ok = (long long)pl.grid * 2 <= (long long)ctx->sms * slab_kernel_occupancy<S>(false);
+  void* warm = (early && reset_in_stream && warm_ok) ? ctx->warm : nullptr;
+  launch_slab_kernel<S>(p, &map, pl.grid, st, reset_in_stream, warm);
   debug_check("slab kernel", st);
   if (ctx->prof_after) record_event(ctx->prof_after, st);
   int launches = reset_in_stream ? 2 : 1;  // + the error-reset kernel
@@ -278,6 +288,7 @@ int build_device(hood_ctx* ctx, const S* pts, long long n, long long block_len, 
     if (early) {
       f.arrive = ctx->arrive;
       f.arrive_target = (unsigned)pl.units;
+      f.warm = warm;
     }
     launch_finalize<S>(f, (int)pl.instances, st, /*pdl=*/!ctx->prof_after);
     debug_check("finalize", st);
@@ -672,6 +683,7 @@ int hood_destroy(hood_ctx* c) {
   cudaFree(c->err);
   cudaFree(c->done);
   cudaFree(c->arrive);
+  cudaFree(c->warm);
   cudaFree(c->rec);
   cudaFree(c->gathered);
   cudaFree(c->d_in);

@@ -153,9 +153,29 @@ __device__ __noinline__ void report_bad(const typename PointT<S>::V* gpts, int n
 // kernel is its programmatic dependent, starts at once and waits for it
 // (griddepcontrol.wait) only on its rare error paths, right before they touch
 // the record.  A memset node in its place costs the step a full node gap.
-__global__ void err_reset_kernel(DevError* err) {
+// It also (re)writes the finalize's warm-up instance (warm != nullptr), so
+// that instance is in L2 when the finalize merges it: two units of three
+// corners, both candidates, six survivors (the small path end to end).
+template <class S>
+__global__ void err_reset_kernel(DevError* err, void* warm) {
+  using V = typename PointT<S>::V;
   asm volatile("griddepcontrol.launch_dependents;");
   err->key = ~0ULL;
+  if (warm) {
+    unsigned char* w = reinterpret_cast<unsigned char*>(warm);
+    V* c = reinterpret_cast<V*>(w);
+    const S xs[6] = {(S)0.1, (S)0.2, (S)0.3, (S)0.6, (S)0.7, (S)0.8};
+    const S ys[6] = {(S)0.1, (S)0.5, (S)0.2, (S)0.3, (S)0.6, (S)0.1};
+    for (int i = 0; i < 6; ++i) c[i] = make_vec<V>(xs[i], ys[i]);
+    int* cnt = reinterpret_cast<int*>(w + 96);
+    cnt[0] = cnt[1] = 3;
+    V* apt = reinterpret_cast<V*>(w + 112);
+    apt[0] = c[1];
+    apt[1] = c[4];
+    long long* base = reinterpret_cast<long long*>(w + 144);
+    base[0] = 0;
+    base[1] = 3;
+  }
 }
 __device__ __forceinline__ void err_ready() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
@@ -1458,7 +1478,7 @@ constexpr int kFinCandCap = 32;    // corners staged per candidate
 //      strict upper hull.
 // Huge survivor sets (the arc) merge the slab hoods in place in HBM instead.
 template <class S>
-__device__ __forceinline__ void finalize_body(const FinalizeParams<S>& p) {
+__device__ __noinline__ void finalize_body(const FinalizeParams<S> p) {
   using V = typename PointT<S>::V;
   constexpr int NWP = kFinThreads / 32;
   constexpr int R = kMaxSlabsPerInstance / kFinThreads;  // segments per thread (at most)
@@ -1497,7 +1517,9 @@ __device__ __forceinline__ void finalize_body(const FinalizeParams<S>& p) {
   V* F = reinterpret_cast<V*>(smem_raw + o_stg + (size_t)MAXC * CAP * sizeof(double2));  // [2][fcap]
 
   if (p.trace && threadIdx.x == 0) p.trace[29] = (long long)gtimer();  // resident
-  if (p.arrive) {
+  if (p.dry) {
+    // the warm-up instance: no waits
+  } else if (p.arrive) {
     // every unit published (the ring kernel's warps may still be exiting):
     // this skips the wait for the ring grid's completion
     if (tid == 0) {
@@ -1830,6 +1852,23 @@ __device__ __forceinline__ void finalize_body(const FinalizeParams<S>& p) {
 
 template <class S>
 __global__ void __launch_bounds__(kFinThreads, 1) finalize_kernel(const FinalizeParams<S> p) {
+  if (p.warm) {
+    // merge the resident dummy instance first: the real merge then runs from
+    // warm instruction caches (after an L2 flush its code comes from DRAM)
+    unsigned char* w = reinterpret_cast<unsigned char*>(p.warm);
+    FinalizeParams<S> d{};
+    d.out = w;
+    d.out_counts = reinterpret_cast<int*>(w + 160);
+    d.seg_cnt = reinterpret_cast<const int*>(w + 96);
+    d.seg_apt = w + 112;
+    d.seg_base = reinterpret_cast<const long long*>(w + 144);
+    d.slabs_per_inst = 2;
+    d.L = 6;
+    d.fcap = p.fcap;
+    d.dry = 1;
+    finalize_body<S>(d);
+    __syncthreads();
+  }
   finalize_body<S>(p);
   // a finalize that started on the unit count (p.arrive) completes only after
   // the ring grid does, so stream order after it covers both kernels
@@ -2152,7 +2191,8 @@ int instance_kernel_occupancy() {
 }
 
 template <class S>
-void launch_slab_kernel(const SlabParams<S>& p, const CUtensorMap* tmap, int grid, cudaStream_t st, bool reset_err) {
+void launch_slab_kernel(const SlabParams<S>& p, const CUtensorMap* tmap, int grid, cudaStream_t st, bool reset_err,
+                        void* warm) {
   if (!p.hmode) {
     instance_kernel_occupancy<S>();
     instance_hull_kernel<S><<<grid, kThreads, inst_smem_bytes<S>(), st>>>(*tmap, p);
@@ -2160,7 +2200,7 @@ void launch_slab_kernel(const SlabParams<S>& p, const CUtensorMap* tmap, int gri
   }
   // reset_err: the error record is reset by a one-thread kernel ahead of the
   // ring kernel, which follows it as a programmatic dependent
-  if (reset_err) err_reset_kernel<<<1, 1, 0, st>>>(p.err);
+  if (reset_err) err_reset_kernel<S><<<1, 1, 0, st>>>(p.err, warm);
   slab_kernel_occupancy<S>(p.lean != 0);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
@@ -2234,8 +2274,9 @@ void launch_pad_fill(void* padded, const void* corners, const int* counts, long 
                                                    reinterpret_cast<const V*>(corners), counts, n, L);
 }
 
-template void launch_slab_kernel<float>(const SlabParams<float>&, const CUtensorMap*, int, cudaStream_t, bool);
-template void launch_slab_kernel<double>(const SlabParams<double>&, const CUtensorMap*, int, cudaStream_t, bool);
+template void launch_slab_kernel<float>(const SlabParams<float>&, const CUtensorMap*, int, cudaStream_t, bool, void*);
+template void launch_slab_kernel<double>(const SlabParams<double>&, const CUtensorMap*, int, cudaStream_t, bool,
+                                         void*);
 template void launch_finalize<float>(const FinalizeParams<float>&, int, cudaStream_t, bool);
 template void launch_finalize<double>(const FinalizeParams<double>&, int, cudaStream_t, bool);
 template void launch_pack_record<float>(const void*, const int*, long long, double, double*, cudaStream_t);

@@ -75,13 +75,19 @@ struct FinalizeParams {
   // ring grid's completion; the finalize zeroes it for the next build
   unsigned* arrive;
   unsigned arrive_target;
+  // optional: a tiny resident dummy instance (kWarmBytes, written by the
+  // error-reset kernel) the finalize merges first, while it waits for the
+  // unit counter -- its code is then in the caches for the real merge
+  void* warm;
+  int dry;                  // internal: this is the dummy run (no waits)
 };
+constexpr int kWarmBytes = 256;
 
 template <class S>
 // reset_err (ring path only): reset the error record in a kernel the ring
 // kernel follows programmatically, instead of a memset node
 void launch_slab_kernel(const SlabParams<S>& p, const CUtensorMap* tmap, int grid, cudaStream_t st,
-                        bool reset_err = false);
+                        bool reset_err = false, void* warm = nullptr);
 void launch_stream_read(const void* p, long long bytes, float* sink, int sms, cudaStream_t st);
 template <class S>
 void launch_finalize(const FinalizeParams<S>& p, int instances, cudaStream_t st, bool pdl = false);
