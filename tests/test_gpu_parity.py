@@ -614,3 +614,18 @@ def test_finished_unit_counter_across_builds(oracle_mod):
         torch.cuda.synchronize()
         assert same(corners[: int(counts[0])].cpu().numpy(), want[0])
         assert same(H.build_hood(ts[1]).hull.cpu().numpy(), want[1])
+
+
+def test_bare_read_reference_kernel_runs():
+    """bench.py's attainable-read reference (hood_internal_stream_read): it
+    launches, reads the whole buffer and leaves it untouched."""
+    import ctypes
+    t = torch.rand(1 << 20, 2, device="cuda")
+    before = t.clone()
+    ctx = H.Context.get(0)
+    s = torch.cuda.current_stream()
+    rc = H.library().hood_internal_stream_read(ctx.handle, ctypes.c_void_p(t.data_ptr()),
+                                               ctypes.c_longlong(t.numel() * 4), ctypes.c_void_p(s.cuda_stream))
+    torch.cuda.synchronize()
+    assert rc == 0 and torch.equal(t, before)
+    assert H.library().hood_internal_stream_read(ctx.handle, None, ctypes.c_longlong(64), None) != 0
