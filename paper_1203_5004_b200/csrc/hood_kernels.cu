@@ -1477,6 +1477,41 @@ constexpr int kFinCandCap = 32;    // corners staged per candidate
 //      (oracle.cpp:7-20, geom.hpp:22-28 predicate in canonical order): the
 //      strict upper hull.
 // Huge survivor sets (the arc) merge the slab hoods in place in HBM instead.
+// The run of hood h[0..c) strictly above chord A-C, as [l, r): the height
+// above the chord is unimodal along a hood, so its peak is found by a binary
+// search on the slope and the run's ends by two more.  One out-of-line copy
+// (the finalize calls it per slab of an unrolled loop; the arc path is cold
+// code after an L2 flush, and four inlined copies cost instruction fetches).
+template <class V>
+__device__ __noinline__ void chord_run(const V* h, int c, V A, V Cp, int& l, int& r) {
+  int a = 0, bq = c - 1;
+  while (a < bq) {
+    const int mid = (a + bq) >> 1;
+    const V d = V{h[mid].x + (Cp.x - A.x), h[mid].y + (Cp.y - A.y)};
+    if (orient_sign(h[mid], h[mid + 1], d) > 0) a = mid + 1;
+    else bq = mid;
+  }
+  const int pk = a;
+  if (!above(A, h[pk], Cp)) {
+    l = r = 0;
+    return;
+  }
+  int x0 = 0, x1 = pk;
+  while (x0 < x1) {
+    const int mid = (x0 + x1) >> 1;
+    if (above(A, h[mid], Cp)) x1 = mid;
+    else x0 = mid + 1;
+  }
+  l = x0;
+  int y0 = pk, y1 = c - 1;
+  while (y0 < y1) {
+    const int mid = (y0 + y1 + 1) >> 1;
+    if (above(A, h[mid], Cp)) y0 = mid;
+    else y1 = mid - 1;
+  }
+  r = y0 + 1;
+}
+
 template <class S>
 __device__ __noinline__ void finalize_body(const FinalizeParams<S> p) {
   using V = typename PointT<S>::V;
@@ -1732,34 +1767,8 @@ __device__ __noinline__ void finalize_body(const FinalizeParams<S> p) {
       const V A = aA[j], Cp = aC[j];
       const V* h = gout + sb[j];
       const int c = sc[j];
-      if (c > 0 && A.y > NEG && Cp.y > NEG && !(above(A, e0[j], Cp) && above(A, e1[j], Cp))) {
-        int a = 0, bq = c - 1;
-        while (a < bq) {
-          const int mid = (a + bq) >> 1;
-          const V d = V{h[mid].x + (Cp.x - A.x), h[mid].y + (Cp.y - A.y)};
-          if (orient_sign(h[mid], h[mid + 1], d) > 0) a = mid + 1;
-          else bq = mid;
-        }
-        const int pk = a;
-        if (!above(A, h[pk], Cp)) {
-          l = r = 0;
-        } else {
-          int x0 = 0, x1 = pk;
-          while (x0 < x1) {
-            const int mid = (x0 + x1) >> 1;
-            if (above(A, h[mid], Cp)) x1 = mid;
-            else x0 = mid + 1;
-          }
-          l = x0;
-          int y0 = pk, y1 = c - 1;
-          while (y0 < y1) {
-            const int mid = (y0 + y1 + 1) >> 1;
-            if (above(A, h[mid], Cp)) y0 = mid;
-            else y1 = mid - 1;
-          }
-          r = y0 + 1;
-        }
-      }
+      if (c > 0 && A.y > NEG && Cp.y > NEG && !(above(A, e0[j], Cp) && above(A, e1[j], Cp)))
+        chord_run<V>(h, c, A, Cp, l, r);
       nsd[s] = sb[j] + l;
       ncd[s] = r - l;
     }
