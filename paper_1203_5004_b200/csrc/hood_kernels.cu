@@ -1424,12 +1424,27 @@ __device__ __forceinline__ void block_excl_argmax2(V v, V ident, V* shV, V& pre,
   if (lane == 31) shV[warp] = up;
   if (lane == 0) shV[NWP + warp] = dn;
   __syncthreads();
-  V cu = ident, cd = ident;
+  // the warp totals, combined by every warp with its own shuffle scans (one
+  // smem read per lane instead of NWP dependent compare-selects)
+  static_assert(NWP <= 32, "one warp combines the warp totals");
+  V t = lane < NWP ? shV[lane] : ident, u = lane < NWP ? shV[NWP + lane] : ident;
 #pragma unroll
-  for (int w = 0; w < NWP; ++w) {
-    if (w < warp && shV[w].y > cu.y) cu = shV[w];
-    if (w > warp && shV[NWP + w].y > cd.y) cd = shV[NWP + w];
+  for (int o = 1; o < NWP; o <<= 1) {
+    V a, b;
+    a.x = __shfl_up_sync(0xffffffffu, t.x, o);
+    a.y = __shfl_up_sync(0xffffffffu, t.y, o);
+    b.x = __shfl_down_sync(0xffffffffu, u.x, o);
+    b.y = __shfl_down_sync(0xffffffffu, u.y, o);
+    if (lane >= o && a.y > t.y) t = a;
+    if (lane + o < NWP && b.y > u.y) u = b;
   }
+  V cu, cd;  // highest of the warps before / after this one
+  cu.x = __shfl_sync(0xffffffffu, t.x, warp > 0 ? warp - 1 : 0);
+  cu.y = __shfl_sync(0xffffffffu, t.y, warp > 0 ? warp - 1 : 0);
+  cd.x = __shfl_sync(0xffffffffu, u.x, warp + 1 < NWP ? warp + 1 : 0);
+  cd.y = __shfl_sync(0xffffffffu, u.y, warp + 1 < NWP ? warp + 1 : 0);
+  if (warp == 0) cu = ident;
+  if (warp + 1 == NWP) cd = ident;
   pre = eu.y > cu.y ? eu : cu;
   suf = ed.y > cd.y ? ed : cd;
 }
@@ -1446,11 +1461,15 @@ __device__ __forceinline__ int block_excl_sum(int v, int* sh, int* total) {
   }
   if (lane == 31) sh[warp] = inc;
   __syncthreads();
-  int carry = 0, tot = 0;
-  for (int w = 0; w < NWP; ++w) {
-    if (w < warp) carry += sh[w];
-    tot += sh[w];
+  // every warp scans the warp totals with shuffles
+  int t = lane < NWP ? sh[lane] : 0;
+#pragma unroll
+  for (int o = 1; o < NWP; o <<= 1) {
+    const int a = __shfl_up_sync(0xffffffffu, t, o);
+    if (lane >= o) t += a;
   }
+  const int carry = warp > 0 ? __shfl_sync(0xffffffffu, t, warp - 1) : 0;
+  const int tot = __shfl_sync(0xffffffffu, t, NWP - 1);
   __syncthreads();
   *total = tot;
   return carry + inc - v;
