@@ -1692,6 +1692,59 @@ __device__ __noinline__ void finalize_body(const FinalizeParams<S> p) {
     }
     __syncthreads();
     if (p.trace && tid == 0) p.trace[3] = clock64();
+    static_assert(CAP == 32, "one lane per staged corner");
+    if (C <= 32) {
+      // the common case, without another CTA barrier: every warp reads the
+      // staged counts and decides alike; when no run overflowed and at most 64
+      // corners survived, warp 0 alone gathers them (a shuffle search of the
+      // run offsets per point), hulls them and writes the hood -- the other
+      // warps are done
+      const int mine = lane < C ? cn[lane] : 0;
+      const int m = min(mine, CAP);
+      int incl = m;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int a = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += a;
+      }
+      const int A = __shfl_sync(0xffffffffu, incl, 31);
+      if (!__any_sync(0xffffffffu, mine > CAP) && A <= 64) {
+        if (warp != 0) return;
+        if (p.trace && lane == 0) p.trace[4] = clock64();
+        const int off = incl - m;  // first survivor of candidate `lane`
+        double2* Hd = reinterpret_cast<double2*>(F);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int i = lane + 32 * k;
+          int c = 0, oc = 0;  // the last candidate whose run starts at or before i
+#pragma unroll
+          for (int st = 16; st >= 1; st >>= 1) {
+            const int cc2 = c + st;
+            const int o2 = __shfl_sync(0xffffffffu, off, cc2 < 32 ? cc2 : 31);
+            if (cc2 < C && o2 <= i) {
+              c = cc2;
+              oc = o2;
+            }
+          }
+          if (i < A) Hd[i] = stg[c * CAP + (i - oc)];
+        }
+        __syncwarp();
+        if (p.trace && lane == 0) p.trace[10] = clock64();
+        const int h = A ? warp_hull_small<double2>(Hd, A, Hd) : 0;
+        if (p.trace && lane == 0) p.trace[11] = p.trace[5] = clock64();
+        for (int e = lane; e < h; e += 32) gout[ibase + e] = make_vec<V>((S)Hd[e].x, (S)Hd[e].y);
+        if (lane == 0) {
+          p.out_counts[blockIdx.x] = h;
+          if (p.trace) {
+            p.trace[6] = p.trace[7] = clock64();
+            p.trace[8] = A;
+            p.trace[9] = C;
+            p.trace[31] = (long long)gtimer();
+          }
+        }
+        return;
+      }
+    }
     // staged counts, their offsets and the overflow flag (a run longer than
     // CAP was truncated) in one block scan: overflows count in bits 20+
     int sum_all = 0;
@@ -1713,7 +1766,6 @@ __device__ __noinline__ void finalize_body(const FinalizeParams<S> p) {
         // (CAP == 32); cc (corner counts) is free after the staging
         if (tid < C) cc[tid] = o0;
         __syncthreads();
-        static_assert(CAP == 32, "one lane per staged corner");
         for (int c = warp; c < C; c += NWP)
           if (lane < min(cn[c], CAP)) Hd[cc[c] + lane] = stg[c * CAP + lane];
         __syncthreads();
