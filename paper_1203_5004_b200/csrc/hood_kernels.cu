@@ -1449,8 +1449,10 @@ __device__ __forceinline__ void block_excl_argmax2(V v, V ident, V* shV, V& pre,
   suf = ed.y > cd.y ? ed : cd;
 }
 
-// Block-wide exclusive prefix sum (blockDim = 32 * NWP).
-template <int NWP>
+// Block-wide exclusive prefix sum (blockDim = 32 * NWP).  Trailing = false
+// skips the closing barrier when sh is not touched again before the caller's
+// next __syncthreads.
+template <int NWP, bool Trailing = true>
 __device__ __forceinline__ int block_excl_sum(int v, int* sh, int* total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int inc = v;
@@ -1470,7 +1472,7 @@ __device__ __forceinline__ int block_excl_sum(int v, int* sh, int* total) {
   }
   const int carry = warp > 0 ? __shfl_sync(0xffffffffu, t, warp - 1) : 0;
   const int tot = __shfl_sync(0xffffffffu, t, NWP - 1);
-  __syncthreads();
+  if (Trailing) __syncthreads();
   *total = tot;
   return carry + inc - v;
 }
@@ -1642,7 +1644,7 @@ __device__ __noinline__ void finalize_body(const FinalizeParams<S> p) {
     }
   }
   int C;
-  int cpos = block_excl_sum<NWP>(ncand, shI, &C);
+  int cpos = block_excl_sum<NWP, false>(ncand, shI, &C);  // next shI use follows a barrier
   if (p.trace && tid == 0) p.trace[2] = clock64();
 
   if (C <= MAXC) {
