@@ -4,17 +4,24 @@
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
 
 A "step" is one build of the hood of one synthetic x-sorted point set that is
-already resident in HBM.  At N=1 the workload is config 2 (n = 2^24 uniform
-points on the 2^-24 float grid, float2 storage); under torchrun (N>1) every
-rank owns one contiguous x-slab of 2^24 points (weak scaling) and the step is
-slab build -> NCCL all_gather of the slab hoods -> final merge on every rank.
+already resident in HBM.  The default workload is config 4, the one the
+north-star target is quoted on: n = 2^28 Gaussian points, x-sorted, double2
+storage (float2 cannot hold 2^28 strictly increasing Gaussian x, SURVEY.md
+F6).  Under torchrun (N>1) the SAME global set is cut into N contiguous
+x-slabs, one per rank (strong scaling; --log2n 30 for the 2^30 run), and the
+step is slab build -> NCCL all_gather of the slab hoods -> final merge on
+every rank.  --config 1|2|3|5 selects the other BASELINE.json configs.
 
 value     = points of all ranks / step time (max over ranks), Gpoints/s
 e2e       = the same metric through the host-pointer C-ABI call
-            (hood_build_host_*: pinned host points -> H2D -> build -> D2H of
-            counts + corners), host copies inside the timed region
-roofline  = slab kernel (the dominant kernel): algorithmic bytes (8 B/pt
-            float2) / its CUDA-event duration, vs MEASURED_PEAKS.json hbm_gbs
+            (hood_build_host_*: host points -> H2D -> build -> D2H of counts
+            + corners), host copies inside the timed region; from pinned host
+            memory (the contract), and from pageable memory (what a
+            std::vector caller hands the drop-in) under e2e.pageable
+roofline  = ring kernel (the dominant kernel): algorithmic bytes (16 B/pt
+            double2, 8 B/pt float2) / its CUDA-event duration, vs
+            MEASURED_PEAKS.json hbm_gbs; frac_8n = the north star's 8n-byte
+            definition (capped at 0.5 for double2 storage)
 cpu_baseline = the reference's own oracle::upper_hull (oracle/_ref, compiled
             from /root/reference sources) on one host core, full workload
 
@@ -32,6 +39,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -46,9 +55,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
-    ap.add_argument("--log2n", type=int, default=None, help="override n for configs 2/4")
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--log2n", type=int, default=None, help="override the global n for configs 2/4")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--e2e-steps", type=int, default=None,
+                    help="timed e2e iterations (default: --steps, at most 20 above 1 GiB of input)")
     ap.add_argument("--no-kernel-events", action="store_true",
                     help="capture the step graph without the event pair around the slab kernel (roofline unmeasured)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -190,26 +201,69 @@ def cpu_reference_batched_rate(points_np, block, seconds, threads):
     return pts.shape[0] / statistics.median(times) / 1e9, kind, len(times)
 
 
+# ---------------------------------------------------------------- shared
+
+def cpu_model() -> str:
+    """lscpu's model name (from /proc/cpuinfo) of the host the CPU legs run on."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_config(args, world: int) -> dict:
+    """The config dict both arms print (identical by construction)."""
+    desc, n, storage, block, _ = workload(args.config, args.log2n)
+    bpp = 16 if storage == "double2" else 8
+    if world > 1:
+        par = (f"x-slab dp{world}: one global set cut into {world} contiguous slabs, "
+               f"NCCL all-gather of the slab hoods + merge" if not block else
+               f"dp{world}: the instances split over {world} GPUs (independent objects, no exchange)")
+    else:
+        par = "single GPU"
+    return {"workload": desc, "n": n, "n_per_rank": n // world, "storage": storage, "bytes_per_point": bpp,
+            "block_len": block or n,
+            "l2": "flushed between timed steps (256 MiB write, then 256 MiB read of another buffer)",
+            "predicate": "reference double orient (geom.hpp:22-28), no FMA; certified f32 filter for float2",
+            "parallelism": par}
+
+
+def make_points_host(args):
+    """The workload as a float64 numpy array, built by the same generator our
+    arm uses (on the GPU when there is one, so both arms see identical points;
+    the generator is not timed)."""
+    import torch
+    _, n, _, _, make = workload(args.config, args.log2n)
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    t = make(dev)
+    out = t.cpu().numpy().astype(np.float64) if t.dtype != torch.float64 else t.cpu().numpy()
+    del t
+    if dev == "cuda":
+        torch.cuda.empty_cache()
+    return out
+
+
 # ---------------------------------------------------------------- reference arm
 
 def run_reference(args):
+    """The reference's own CPU implementation of the path (oracle/_ref: the
+    unmodified reference oracle::upper_hull, slab-parallel on every host
+    thread -- SURVEY.md A10 -- or per instance for the batched config) on the
+    FULL workload every step."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
-    import numpy as np
     desc, n, storage, block, make = workload(args.config, args.log2n)
-    pts = make("cpu").numpy()
+    p64 = np.ascontiguousarray(make_points_host(args), dtype=np.float64)
     threads = os.cpu_count() or 1
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
     kind = "reference" if O.ref_available() else "port"
-    # each step is a bounded sample of the workload (the first 2^24 points --
-    # whole instances when batched), so the full --steps/--warmup run stays
-    # within minutes even for the 2^28 config; the rate is points / time
-    SAMPLE = 1 << 24
-    p64 = np.ascontiguousarray(pts[:SAMPLE], dtype=np.float64)
-    m = p64.shape[0]
-    N = args.gpus
 
     def step():
         if block:
@@ -225,24 +279,23 @@ def run_reference(args):
 
     for _ in range(args.warmup):
         step()
-    t0 = time.perf_counter()
+    times = []
     for _ in range(args.steps):
+        t0 = time.perf_counter()
         step()
-    dt = (time.perf_counter() - t0) / args.steps
-    # Weak scaling: the reference has no multi-node layer; N slabs of n points
-    # on the same host cores cost N x the single-slab time.
-    value = m / dt / 1e9
+        times.append(time.perf_counter() - t0)
+    dt = statistics.mean(times)
+    value = n / dt / 1e9
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 * N * n / m,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": desc, "n_per_rank": n, "storage": storage,
-                                        "block_len": block or n},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": (f"full workload per step ({n} points), " if m == n else
-                                    f"first {m} of {n} points per step (rate = points / time), ")
-                                   + f"{'oracle/_ref' if kind == 'reference' else 'oracle port'} "
-                                   + f"{'block' if block else 'slab'}-parallel upper_hull on {threads} threads"},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "config": run_config(args, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "cpu_model": cpu_model(),
+                         "sample": f"full workload every step ({n} points), "
+                                   + f"{'oracle/_ref (unmodified reference oracle::upper_hull)' if kind == 'reference' else 'oracle port'} "
+                                   + (f"one upper_hull per {block}-point instance, instances over {threads} threads"
+                                      if block else f"slab-parallel upper_hull on {threads} threads + hull of the slab hulls")},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -252,7 +305,6 @@ def run_reference(args):
 # ---------------------------------------------------------------- our arm
 
 def run_ours(args):
-    import numpy as np
     import torch
     import torch.distributed as dist
     from paper_1203_5004_b200 import hood as H
@@ -269,8 +321,15 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
 
-    desc, n, storage, block, make = workload(args.config, args.log2n)
-    pts = make(dev)
+    desc, n_global, storage, block, make = workload(args.config, args.log2n)
+    # this rank's contiguous slab of the one global set (x already global)
+    full = make(dev)
+    n = n_global // world
+    if block and n % block:
+        raise SystemExit(f"{n_global // block} instances do not split over {world} ranks")
+    pts = full[rank * n:(rank + 1) * n].clone() if world > 1 else full
+    del full
+    torch.cuda.empty_cache()
     f64 = pts.dtype == torch.float64
     bpp = 16 if f64 else 8
     ctx = H.Context.get(local)
@@ -290,8 +349,8 @@ def run_ours(args):
         torch.amax(drain, dim=0, out=sink)
     stream = torch.cuda.current_stream(dev)
 
-    # multi-GPU exchange buffers (slab hoods in global double coordinates)
-    CAP = 512  # slab hood corners per exchange record (random slabs: ~30)
+    # multi-GPU exchange buffers (slab hoods, global double coordinates)
+    CAP = 512 if args.config != 3 else n  # slab hood corners per record (random slabs: ~30; arc: all)
     # batched instances (config 5) are independent objects: no exchange
     exchange_slabs = multi and not block
     if exchange_slabs:
@@ -301,10 +360,10 @@ def run_ours(args):
         final_cnt = torch.empty(1, dtype=torch.int32, device=dev)
 
     def exchange():
-        # slab r lives at x in (r, r+1): its hood goes into global double
-        # coordinates (exact) in one pack kernel, the records are gathered
-        # over NCCL, and every rank merges them (paper_1203_5004_b200/distributed.py)
-        H.pack_record(corners, counts, CAP, x_offset=float(rank), rec=rec)
+        # the slab hood (already in global x) into one record, records
+        # gathered over NCCL, every rank merges them
+        # (paper_1203_5004_b200/distributed.py)
+        H.pack_record(corners, counts, CAP, x_offset=0.0, rec=rec)
         dist.all_gather_into_tensor(gathered.view(-1), rec.view(-1))
         H.merge_records(gathered, out=final, out_count=final_cnt)
 
@@ -322,8 +381,10 @@ def run_ours(args):
     # overflow of the exchange) before anything is timed
     one_step()
     ctx.last_error()
-    if exchange_slabs and int(counts[0]) > CAP:
-        raise RuntimeError("slab hood exceeds the exchange record capacity")
+    if exchange_slabs:
+        ctx.last_error()
+        if int(counts[0]) > CAP:
+            raise RuntimeError("slab hood exceeds the exchange record capacity")
 
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -333,17 +394,15 @@ def run_ours(args):
         e.record(stream)
     torch.cuda.synchronize()
 
-    # One build = one CUDA graph replay on a single GPU (the C-ABI builds are
-    # capture-safe): the timed region then holds the kernels and nothing of the
-    # Python / ctypes launch path.  The timed steps run a plain graph; the
-    # roofline comes from a second pass over a graph whose slab kernel is
-    # bracketed by a captured event pair (events inside the graph cost a few
-    # microseconds of step time, so they stay out of the timed steps).
-    # Multi-GPU steps (NCCL exchange) run eagerly.
+    # One step = one CUDA graph replay (the C-ABI builds, the NCCL all-gather
+    # and the merge are capture-safe): the timed region holds the kernels and
+    # nothing of the Python / ctypes launch path.  The timed steps run a plain
+    # graph; the roofline comes from a second pass over a graph whose ring
+    # kernel is bracketed by a captured event pair (events inside the graph
+    # cost a few microseconds of step time, so they stay out of the timed
+    # steps).
     graph = prof_graph = None
     if not multi or os.environ.get("HOOD_BENCH_EAGER") != "1":
-        # multi-GPU steps are captured too: the NCCL all-gather and the merge
-        # are graph-safe, so a step is one replay on every rank
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             one_step()
@@ -381,7 +440,7 @@ def run_ours(args):
     if multi:
         dist.barrier()
     torch.cuda.synchronize()
-    # roofline pass: the slab kernel alone, event-timed on its own stream
+    # roofline pass: the ring kernel alone, event-timed on its own stream
     kern_ms = []
     if not args.no_kernel_events:
         for i in range(args.steps):
@@ -427,37 +486,51 @@ def run_ours(args):
         ms, kms = float(t[0]), float(t[1])
     value = world * n / (ms * 1e-3) / 1e9
 
-    # ---- e2e through the host-pointer C-ABI call
+    # ---- e2e through the host-pointer C-ABI call (what a reference caller
+    # does: points in host memory in, compact corners back in host memory)
     e2e = None
     if not args.no_e2e:
-        host = pts.cpu().pin_memory()
-        out_h = torch.empty_like(host).pin_memory()
+        e_steps = args.e2e_steps or (args.steps if n * bpp <= (1 << 30) else min(args.steps, 20))
+        out_h = torch.empty_like(pts, device="cpu").pin_memory()
         cnt_h = torch.zeros(inst, dtype=torch.int32).pin_memory()
-        e_times = []
-        for i in range(args.warmup + args.steps):
+
+        def e2e_run(host):
+            times = []
+            for i in range(args.warmup + e_steps):
+                if multi:
+                    dist.barrier()
+                t0 = time.perf_counter()
+                rc = H.build_hood_host_ptr(ctx, host.data_ptr(), n, f64, out_h.data_ptr(), cnt_h.data_ptr(), block)
+                if rc:
+                    raise RuntimeError(f"host build failed: {rc}")
+                if exchange_slabs:
+                    corners[: int(cnt_h[0])].copy_(out_h[: int(cnt_h[0])], non_blocking=True)
+                    counts[0] = int(cnt_h[0])
+                    exchange()
+                    final_cnt.item()
+                if i >= args.warmup:
+                    times.append(time.perf_counter() - t0)
+            e_ms = statistics.mean(times) * 1e3
             if multi:
-                dist.barrier()
-            t0 = time.perf_counter()
-            rc = H.build_hood_host_ptr(ctx, host.data_ptr(), n, f64, out_h.data_ptr(), cnt_h.data_ptr(), block)
-            if rc:
-                raise RuntimeError(f"host build failed: {rc}")
-            if exchange_slabs:
-                corners[: int(cnt_h[0])].copy_(out_h[: int(cnt_h[0])], non_blocking=True)
-                counts[0] = int(cnt_h[0])
-                exchange()
-                final_cnt.item()
-            if i >= args.warmup:
-                e_times.append(time.perf_counter() - t0)
-        e_ms = statistics.mean(e_times) * 1e3
-        if multi:
-            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t[0])
+                t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                e_ms = float(t[0])
+            return e_ms
+
+        pageable = pts.cpu()  # plain (pageable) host memory, like a std::vector
+        pg_ms = e2e_run(pageable)
+        pinned = pageable.pin_memory()
+        del pageable
+        e_ms = e2e_run(pinned)
+        del pinned
         # counts + corners as hood_build_host copies them (batched: one
         # strided copy of the widest instance's count per instance)
         d2h = inst * 4 + (int(cnt_h.max()) * inst if inst > 1 else int(cnt_h[0])) * bpp
-        e2e = {"value": world * n / (e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e_ms,
-               "h2d_bytes_per_step": n * bpp, "d2h_bytes_per_step": d2h}
+        e2e = {"value": world * n / (e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e_ms, "steps": e_steps,
+               "h2d_bytes_per_step": world * n * bpp, "d2h_bytes_per_step": world * d2h,
+               "host_memory": "pinned",
+               "pageable": {"value": world * n / (pg_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": pg_ms,
+                            "host_memory": "pageable (plain malloc'd host tensor, as a std::vector caller)"}}
 
     if rank == 0:
         peak, peak_src = peaks()
@@ -476,22 +549,22 @@ def run_ours(args):
                 rate, kind, reps = cpu_reference_batched_rate(hostpts, block, args.cpu_seconds, 1)
             else:
                 rate, kind, reps = cpu_reference_rate(hostpts, args.cpu_seconds, 1)
-            cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": kind,
+            del hostpts
+            cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": kind, "cpu_model": cpu_model(),
+                   "host_threads": os.cpu_count(),
                    "sample": f"full workload ({n} points) x {reps} runs (median), "
                              f"{'oracle/_ref = reference oracle::upper_hull' if kind == 'reference' else 'C port'}"
                              f", single thread, same input"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": desc, "n_per_rank": n, "storage": storage, "bytes_per_point": bpp,
-                       "block_len": block or n, "l2": "flushed between timed steps (256 MiB write, then 256 MiB read of another buffer)",
-                       "predicate": "reference double orient, certified f32 filter",
-                       "parallelism": (f"x-slab dp{world}, NCCL all-gather of slab hoods + merge" if exchange_slabs
-                                       else f"{world} GPUs, independent instances" if multi else "single GPU")},
+            "config": run_config(args, world),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(args.config),
+                         "frac_8n": (n * 8 / (kms * 1e-3) / 1e9) / peak,
                          "kernel": "ring_hull_kernel", "kernel_ms": kms,
                          "algorithmic_bytes_per_launch": n * bpp, "peak_source": peak_src,
                          "bare_read": bare_read},

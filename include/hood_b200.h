@@ -36,7 +36,7 @@ typedef enum hood_status {
   HOOD_ERR_INVALID_ARG = 1,      /* bad size / alignment / block_len     */
   HOOD_ERR_X_NOT_INCREASING = 2, /* ValidationError::x_not_increasing    */
   HOOD_ERR_X_OUT_OF_RANGE = 3,   /* ValidationError::x_out_of_range      */
-  HOOD_ERR_DEGENERATE = 4,       /* reserved: DegenerateTangent          */
+  HOOD_ERR_DEGENERATE = 4,       /* DegenerateTangent (hood_merge_round)  */
   HOOD_ERR_CUDA = 5,             /* a CUDA runtime call failed           */
   HOOD_ERR_CAPACITY = 6,         /* workspace / record capacity exceeded */
   HOOD_ERR_NOT_POWER_OF_TWO = 7, /* ValidationError::not_power_of_two    */
@@ -52,7 +52,12 @@ typedef struct hood_error {
 } hood_error;
 
 /* Build flags. */
-#define HOOD_FLAG_CHECK_RANGE 0x1u /* also reject x outside (0, 1) (validate_points) */
+#define HOOD_FLAG_CHECK_RANGE 0x1u   /* also reject x outside (0, 1) (validate_points) */
+#define HOOD_FLAG_CHECK_TRIPLES 0x2u /* also reject consecutive triples (i, i+1, i+2) with
+                                        |orient| < 1e-9 (validate_points' margin check,
+                                        hoodbuf.cpp:53-60; HOOD_ERR_DEGENERATE_TRIPLE,
+                                        index = i), after every x check as the reference
+                                        orders them */
 
 /* One context per device and host thread (the reference build is reentrant,
  * SPEC.md:423; contexts share nothing).  A context owns one device workspace
@@ -84,9 +89,12 @@ int hood_build_f64(hood_ctx* ctx, const double* d_pts, int64_t n, int64_t block_
                    int32_t* d_counts, double* d_padded, uint32_t flags, void* stream);
 
 /* Host-pointer build (the reference-facing call: points in host memory,
- * compact corners back in host memory).  Copies in pinned chunks overlapped
- * with the slab kernels.  Synchronous.  h_corners needs n slots; returns the
- * per-instance counts in h_counts. */
+ * compact corners back in host memory).  Synchronous.  h_corners needs n
+ * slots; returns the per-instance counts in h_counts.  The input goes to the
+ * device in chunks, each chunk's units launched as soon as its bytes land:
+ * pinned (page-locked) input is copied by DMA directly; pageable input (a
+ * std::vector) is staged by host threads through pinned bounce buffers
+ * owned by the context, overlapped with the DMA. */
 int hood_build_host_f32(hood_ctx* ctx, const float* h_pts, int64_t n, int64_t block_len, float* h_corners,
                         int32_t* h_counts, uint32_t flags);
 int hood_build_host_f64(hood_ctx* ctx, const double* h_pts, int64_t n, int64_t block_len,
@@ -106,7 +114,13 @@ int hood_merge_segments_f64(hood_ctx* ctx, const double* d_seg_pts, const int32_
  * then the corners widened to double with x + x_offset -- the records are
  * all-gathered (NCCL), and every rank merges the G records (rank order = x
  * order) into the global hood: d_out (G*cap double2 slots) and d_count.
- * Asynchronous, graph-capturable. */
+ * Asynchronous, graph-capturable.  A slab hood of more than cap corners is
+ * never merged silently: the record keeps the true count in its header, and
+ * hood_last_error() then reports HOOD_ERR_CAPACITY with index = the record
+ * capacity needed (exchange again with records that large; the d_out/d_count
+ * of that merge are not the global hood).  x + x_offset is exact for float2
+ * slabs (float x widened to double plus a small integer offset); double2 slabs
+ * should carry global x already (x_offset 0). */
 int hood_pack_record_f32(hood_ctx* ctx, const float* d_corners, const int32_t* d_count, int64_t cap,
                          double x_offset, double* d_rec, void* stream);
 int hood_pack_record_f64(hood_ctx* ctx, const double* d_corners, const int32_t* d_count, int64_t cap,
@@ -119,8 +133,10 @@ int hood_merge_records(hood_ctx* ctx, const double* d_recs, int64_t G, int64_t c
  * points on its own device, x in slab g's range, slabs left to right, x
  * shifted by x_offsets[g] when given), packs it, the records go peer-to-peer
  * to ctxs[0]'s device, which merges them into d_out (G*cap double2, on
- * ctxs[0]'s device) and d_count.  Synchronous; slab hoods larger than cap
- * corners are truncated (size cap to the expected hoods). */
+ * ctxs[0]'s device) and d_count.  Synchronous.  Records are sized to the
+ * largest slab hood when one exceeds cap (never truncated); HOOD_ERR_CAPACITY
+ * (hood_last_error(ctxs[0]).index = slots needed) only when the global hood
+ * itself has more than G*cap corners. */
 int hood_build_multi_f32(hood_ctx* const* ctxs, int G, const float* const* d_slabs, const int64_t* n_per,
                          const double* x_offsets, double* d_out, int32_t* d_count, int64_t cap);
 int hood_build_multi_f64(hood_ctx* const* ctxs, int G, const double* const* d_slabs, const int64_t* n_per,
@@ -135,8 +151,24 @@ int hood_build_multi_f64(hood_ctx* const* ctxs, int G, const double* const* d_sl
  * `stream`.  The per-round parity seam. */
 int hood_merge_round_f32(hood_ctx* ctx, const float* d_in, int64_t n, int64_t d, float* d_out, void* stream);
 int hood_merge_round_f64(hood_ctx* ctx, const double* d_in, int64_t n, int64_t d, double* d_out, void* stream);
+/* The same round, also leaving the pinpoint phase's result in d_scratch
+ * (n int32, kernel.cpp:101-112): for the pair window starting at slot
+ * start = 2*b*d, d_scratch[start] = pindex and d_scratch[start+1] = qindex,
+ * absolute slot indices of the common tangent's corners (the other entries
+ * are not written).  A pair whose common tangent is not unique -- a corner
+ * next to either end lies exactly on the bridge line, where the reference
+ * throws DegenerateTangent(round, block) or reports the pinpoint's write-write
+ * conflict (kernel.cpp:163-187, test_kernel.cpp:330-350) -- is reported by
+ * hood_last_error() as HOOD_ERR_DEGENERATE with index = the first such block
+ * (all four merge_round entry points check it). */
+int hood_merge_round_scratch_f32(hood_ctx* ctx, const float* d_in, int64_t n, int64_t d, float* d_out,
+                                 int32_t* d_scratch, void* stream);
+int hood_merge_round_scratch_f64(hood_ctx* ctx, const double* d_in, int64_t n, int64_t d, double* d_out,
+                                 int32_t* d_scratch, void* stream);
 
-/* Synchronizes the stream of the last build and reports its first error. */
+/* Synchronizes the stream of the last build and reports its first error:
+ * validation (x range / order, then the consecutive-triple margin) before a
+ * record capacity shortfall (HOOD_ERR_CAPACITY, index = capacity needed). */
 int hood_last_error(hood_ctx* ctx, hood_error* out);
 
 /* Number of kernels the last build enqueued (bench bookkeeping). */

@@ -56,6 +56,9 @@ struct hood_ctx {
   int last_launches = 0;
   int sticky_cuda = 0;
   cudaEvent_t prof_before = nullptr, prof_after = nullptr;
+  cudaEvent_t order_ev = nullptr;  // orders a build on a new stream after the last one
+  void* round_tmp = nullptr;       // merge_round in place: a copy of the input
+  size_t round_tmp_bytes = 0;
   int dbg = 0;
   long long* trace = nullptr;
 };
@@ -205,6 +208,7 @@ SlabParams<S> slab_params(hood_ctx* ctx, const Plan& pl, const void* pts, void* 
   p.seg_base = ctx->seg_base;
   p.err = ctx->err;
   p.check_range = (flags & HOOD_FLAG_CHECK_RANGE) ? 1 : 0;
+  p.check_triples = (flags & HOOD_FLAG_CHECK_TRIPLES) ? 1 : 0;
   p.dbg = ctx->dbg;
   p.trace = ctx->trace;
   p.read_lim = pl.n;
@@ -250,6 +254,25 @@ void record_event(cudaEvent_t ev, cudaStream_t st) {
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+bool capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  return cs != cudaStreamCaptureStatusNone;
+}
+
+// A context's workspace (unit summaries, error record, finished-unit counter)
+// is reused by every build, so a build on another stream than the context's
+// last one is ordered after it (an event edge).  Inside a graph capture the
+// caller orders the replay; a capture-time edge to an uncaptured stream would
+// invalidate the capture, so none is added there.
+void order_after_last(hood_ctx* ctx, cudaStream_t st) {
+  if (!ctx->have_last || ctx->last_stream == st) return;
+  if (capturing(st) || capturing(ctx->last_stream)) return;
+  if (!ctx->order_ev && cudaEventCreateWithFlags(&ctx->order_ev, cudaEventDisableTiming) != cudaSuccess) return;
+  cudaEventRecord(ctx->order_ev, ctx->last_stream);
+  cudaStreamWaitEvent(st, ctx->order_ev, 0);
+}
+
 template <class S>
 int build_device(hood_ctx* ctx, const S* pts, long long n, long long block_len, S* corners, int* counts,
                  S* padded, uint32_t flags, cudaStream_t st) {
@@ -260,6 +283,7 @@ int build_device(hood_ctx* ctx, const S* pts, long long n, long long block_len, 
   int rc = make_plan<S>(ctx, n, block_len, pl);
   if (rc) return rc;
   if ((rc = ensure_ws(ctx, pl.units))) return rc;
+  order_after_last(ctx, st);
   CUtensorMap map;
   long long full_rows = 0;
   std::memset(&map, 0, sizeof(map));  // the stream kernel (hmode) reads with LDG, no tensor map
@@ -318,14 +342,23 @@ int decode_error(hood_ctx* ctx, hood_error* out) {
     ctx->sticky_cuda = 0;
   } else if (ctx->have_last && ctx->err) {
     cudaError_t ce = cudaStreamSynchronize(ctx->last_stream);
-    DevError de{~0ULL};
+    DevError de{~0ULL, -1, ~0ULL};
     if (ce == cudaSuccess) ce = cudaMemcpy(&de, ctx->err, sizeof(de), cudaMemcpyDeviceToHost);
     if (ce != cudaSuccess) {
       e.code = HOOD_ERR_CUDA;
       e.cuda_error = (int)ce;
+    } else if (de.key != ~0ULL && de.key >= kTripleKey) {
+      e.code = HOOD_ERR_DEGENERATE_TRIPLE;  // points (index, index+1, index+2)
+      e.index = (int64_t)(de.key - kTripleKey);
     } else if (de.key != ~0ULL) {
       e.code = (de.key & 1ULL) ? HOOD_ERR_X_NOT_INCREASING : HOOD_ERR_X_OUT_OF_RANGE;
       e.index = (int64_t)(de.key >> 1);
+    } else if (de.need >= 0) {
+      e.code = HOOD_ERR_CAPACITY;  // an exchange record needed `need` corners
+      e.index = (int64_t)de.need;
+    } else if (de.degen != ~0ULL) {
+      e.code = HOOD_ERR_DEGENERATE;  // hood_merge_round: block (pair) index
+      e.index = (int64_t)de.degen;
     }
   }
   if (out) *out = e;
@@ -377,6 +410,7 @@ int build_host(hood_ctx* ctx, const S* h_pts, long long n, long long block_len, 
   std::memset(&map, 0, sizeof(map));
   if (!pl.hmode && (rc = encode_map<S>(d_in, n, pl.rows, &map, &full_rows))) return rc;
   cudaStream_t sc = ctx->s_copy, sk = ctx->s_comp;
+  order_after_last(ctx, sk);
   cudaMemsetAsync(ctx->err, 0xff, sizeof(DevError), sk);
   SlabParams<S> p = slab_params<S>(ctx, pl, d_in, d_out, ctx->d_counts, full_rows, flags);
   const int chunks = (pl.hmode && pl.instances == 1 && pl.units >= hood_ctx::kChunks) ? hood_ctx::kChunks : 1;
@@ -435,6 +469,7 @@ int merge_segments(hood_ctx* ctx, const S* seg_pts, const int* counts, long long
   cudaSetDevice(ctx->device);
   int rc;
   if ((rc = ensure_ws(ctx, G))) return rc;
+  order_after_last(ctx, st);
   if (seg_pts != corners &&
       cudaMemcpyAsync(corners, seg_pts, (size_t)G * stride * sizeof(V), cudaMemcpyDeviceToDevice, st) !=
           cudaSuccess)
@@ -460,33 +495,35 @@ int merge_segments(hood_ctx* ctx, const S* seg_pts, const int* counts, long long
 
 // One round of the reference loop on the GPU: REMOTE-padded blocks of d in,
 // blocks of 2d out (driver.cpp:20-43 with launch(match_and_merge_kernel),
-// kernel.cpp:155-161).  Each pair of adjacent block hoods is merged by the
-// finalize kernel (one CTA per pair), then padded again.
+// kernel.cpp:155-161): the corner count of every block (the non-REMOTE
+// prefix, hoodbuf.cpp:87-92), the common tangent of every pair (optionally
+// left in scratch as the pinpoint phase does), the splice with REMOTE padding.
+// d_in == d_out merges through a copy of the input in the context workspace.
 template <class S>
-int merge_round(hood_ctx* ctx, const S* in, long long n, long long d, S* out, cudaStream_t st) {
+int merge_round(hood_ctx* ctx, const S* in, long long n, long long d, S* out, int* scratch, cudaStream_t st) {
   using V = typename PointT<S>::V;
   if (!ctx || !in || !out) return HOOD_ERR_INVALID_ARG;
   if (d < 1 || (d & (d - 1)) != 0 || n < 2 * d || n % (2 * d) != 0) return HOOD_ERR_INVALID_ARG;
   cudaSetDevice(ctx->device);
   int rc;
   if ((rc = ensure_ws(ctx, n / d))) return rc;
-  if (in != out &&
-      cudaMemcpyAsync(out, in, (size_t)n * sizeof(V), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
-    return HOOD_ERR_CUDA;
-  int* pair_counts = reinterpret_cast<int*>(ctx->seg_base);  // n/(2d) ints, workspace
-  launch_block_count<S>(out, n, d, ctx->seg_cnt, st);
-  FinalizeParams<S> f{};
-  f.out = out;
-  f.out_counts = pair_counts;
-  f.seg_cnt = ctx->seg_cnt;
-  f.seg_apt = nullptr;
-  f.seg_base = nullptr;
-  f.seg_stride = d;
-  f.slabs_per_inst = 2;
-  f.L = 2 * d;
-  f.fcap = (int)(32768 / sizeof(V));
-  launch_finalize<S>(f, (int)(n / (2 * d)), st);
-  launch_pad_fill<S>(out, out, pair_counts, n, 2 * d, st);
+  order_after_last(ctx, st);
+  const size_t bytes = (size_t)n * sizeof(V);
+  if (in == out) {
+    if (bytes > ctx->round_tmp_bytes) {
+      cudaFree(ctx->round_tmp);
+      ctx->round_tmp = nullptr;
+      if (cudaMalloc(&ctx->round_tmp, bytes) != cudaSuccess) return HOOD_ERR_CUDA;
+      ctx->round_tmp_bytes = bytes;
+    }
+    if (cudaMemcpyAsync(ctx->round_tmp, in, bytes, cudaMemcpyDeviceToDevice, st) != cudaSuccess) return HOOD_ERR_CUDA;
+    in = reinterpret_cast<const S*>(ctx->round_tmp);
+  }
+  if (cudaMemsetAsync(ctx->err, 0xff, sizeof(DevError), st) != cudaSuccess) return HOOD_ERR_CUDA;
+  // workspace: block counts (n/d ints) and per-pair (pindex, qindex) (n/(2d) int2)
+  int* pq = reinterpret_cast<int*>(ctx->seg_base);
+  launch_block_count<S>(in, n, d, ctx->seg_cnt, st);
+  launch_round_merge<S>(in, n, d, ctx->seg_cnt, pq, scratch, out, ctx->err, st);
   ctx->last_stream = st;
   ctx->have_last = true;
   ctx->last_launches = 3;
@@ -500,7 +537,10 @@ int pack_record(hood_ctx* ctx, const S* corners, const int* count, long long cap
                 cudaStream_t st) {
   if (!ctx || !corners || !count || !rec || cap < 1) return HOOD_ERR_INVALID_ARG;
   cudaSetDevice(ctx->device);
-  launch_pack_record<S>(corners, count, cap, x_offset, rec, st);
+  int rc;
+  if ((rc = ensure_ws(ctx, 1))) return rc;
+  order_after_last(ctx, st);
+  launch_pack_record<S>(corners, count, cap, x_offset, rec, ctx->err, st);
   ctx->last_stream = st;
   ctx->have_last = true;
   ctx->last_launches = 1;
@@ -514,7 +554,8 @@ int merge_records(hood_ctx* ctx, const double* recs, long long G, long long cap,
   cudaSetDevice(ctx->device);
   int rc;
   if ((rc = ensure_ws(ctx, G))) return rc;
-  launch_gather_records(recs, G, cap, out, ctx->seg_cnt, count, ctx->done, st);
+  order_after_last(ctx, st);
+  launch_gather_records(recs, G, cap, out, ctx->seg_cnt, count, ctx->done, ctx->err, st);
   FinalizeParams<double> f{};
   f.out = out;
   f.out_counts = count;
@@ -534,36 +575,54 @@ int merge_records(hood_ctx* ctx, const double* recs, long long G, long long cap,
 }
 
 // Single-process multi-GPU build (SURVEY.md 8(b) hood_build_multi, the P2P
-// variant of 8(e)): every context builds its slab's hood on its own device
-// and packs its record; the records are copied peer-to-peer (NVLink) to the
-// first context's device, which merges them.  Synchronous.
+// variant of 8(e)): every context builds its slab's hood on its own device,
+// the slab hood sizes are read back, the records (sized to the largest slab
+// hood when one exceeds cap -- the count-sized exchange distributed.py does
+// for the NCCL path; nothing is ever truncated) are packed and copied
+// peer-to-peer (NVLink) to the first context's device, which merges them.
+// Synchronous.  HOOD_ERR_CAPACITY (hood_last_error(ctxs[0]).index = the
+// needed slots) only when the merged hood itself exceeds G*cap.
 template <class S>
 int build_multi(hood_ctx* const* ctxs, int G, const S* const* slabs, const int64_t* n_per, const double* x_off,
                 double* d_out, int* d_count, long long cap) {
-  using V = typename PointT<S>::V;
   if (!ctxs || G < 1 || !slabs || !n_per || !d_out || !d_count || cap < 1) return HOOD_ERR_INVALID_ARG;
   if (G > kMaxSlabsPerInstance) return HOOD_ERR_INVALID_ARG;
   hood_ctx* c0 = ctxs[0];
   int rc;
-  // 1. every slab: build + pack on its own device and stream
+  // 1. every slab: build on its own device and stream
   for (int g = 0; g < G; ++g) {
     hood_ctx* c = ctxs[g];
     if (!c || !slabs[g] || n_per[g] < 1) return HOOD_ERR_INVALID_ARG;
     cudaSetDevice(c->device);
     if ((rc = ensure_host_bufs<S>(c, n_per[g], 1))) return rc;
-    if (c->rec_cap < cap) {
-      cudaFree(c->rec);
-      c->rec = nullptr;
-      if (cudaMalloc(&c->rec, (size_t)(cap + 1) * 2 * sizeof(double)) != cudaSuccess) return HOOD_ERR_CUDA;
-      c->rec_cap = cap;
-    }
     S* corners = reinterpret_cast<S*>(c->d_out);
     if ((rc = build_device<S>(c, slabs[g], n_per[g], 0, corners, c->d_counts, nullptr, 0, c->s_comp))) return rc;
-    launch_pack_record<S>(corners, c->d_counts, cap, x_off ? x_off[g] : 0.0, c->rec, c->s_comp);
   }
-  // 2. the records to the first device, after each slab's stream
+  // 2. the slab hood sizes (and every slab's validation errors)
+  long long rcap = cap;
+  for (int g = 0; g < G; ++g) {
+    hood_error e;
+    if ((rc = decode_error(ctxs[g], &e))) return rc;
+    int k = 0;
+    cudaSetDevice(ctxs[g]->device);
+    if (cudaMemcpy(&k, ctxs[g]->d_counts, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return HOOD_ERR_CUDA;
+    rcap = std::max(rcap, (long long)k);
+  }
+  // 3. records of rcap corners, peer-to-peer to the first device
+  for (int g = 0; g < G; ++g) {
+    hood_ctx* c = ctxs[g];
+    cudaSetDevice(c->device);
+    if (c->rec_cap < rcap) {
+      cudaFree(c->rec);
+      c->rec = nullptr;
+      if (cudaMalloc(&c->rec, (size_t)(rcap + 1) * 2 * sizeof(double)) != cudaSuccess) return HOOD_ERR_CUDA;
+      c->rec_cap = rcap;
+    }
+    launch_pack_record<S>(c->d_out, c->d_counts, rcap, x_off ? x_off[g] : 0.0, c->rec, c->err, c->s_comp);
+  }
   cudaSetDevice(c0->device);
-  const long long need = (long long)G * (cap + 1) * 2;
+  // G records, then (when rcap > cap) G*rcap double2 of merge output
+  const long long need = (long long)G * (rcap + 1) * 2 + (rcap > cap ? (long long)G * rcap * 2 : 0);
   if (c0->gathered_elems < need) {
     cudaFree(c0->gathered);
     c0->gathered = nullptr;
@@ -576,18 +635,28 @@ int build_multi(hood_ctx* const* ctxs, int G, const S* const* slabs, const int64
     cudaEventRecord(c->ev[0], c->s_comp);
     cudaSetDevice(c0->device);
     cudaStreamWaitEvent(c0->s_comp, c->ev[0], 0);
-    cudaMemcpyPeerAsync(c0->gathered + (size_t)g * (cap + 1) * 2, c0->device, c->rec, c->device,
-                        (size_t)(cap + 1) * 2 * sizeof(double), c0->s_comp);
+    cudaMemcpyPeerAsync(c0->gathered + (size_t)g * (rcap + 1) * 2, c0->device, c->rec, c->device,
+                        (size_t)(rcap + 1) * 2 * sizeof(double), c0->s_comp);
   }
-  // 3. merge on the first device
-  if ((rc = merge_records(c0, c0->gathered, G, cap, d_out, d_count, c0->s_comp))) return rc;
+  // 4. merge on the first device; into the caller's buffer when the records
+  // fit its G*cap slots, else into a scratch buffer checked below
+  double* out = rcap > cap ? c0->gathered + (size_t)G * (rcap + 1) * 2 : d_out;
+  if ((rc = merge_records(c0, c0->gathered, G, rcap, out, d_count, c0->s_comp))) return rc;
   if (cudaStreamSynchronize(c0->s_comp) != cudaSuccess) return HOOD_ERR_CUDA;
-  for (int g = 0; g < G; ++g) {  // validation errors of any slab
-    hood_error e;
-    if ((rc = decode_error(ctxs[g], &e))) return rc;
+  if (out != d_out) {
+    int h = 0;
+    if (cudaMemcpy(&h, d_count, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return HOOD_ERR_CUDA;
+    if (h > (long long)G * cap) {
+      DevError de{~0ULL, (long long)h, ~0ULL};
+      cudaMemcpy(c0->err, &de, sizeof(de), cudaMemcpyHostToDevice);
+      c0->have_last = true;
+      return HOOD_ERR_CAPACITY;
+    }
+    if (cudaMemcpy(d_out, out, (size_t)h * 2 * sizeof(double), cudaMemcpyDeviceToDevice) != cudaSuccess)
+      return HOOD_ERR_CUDA;
   }
-  (void)sizeof(V);
-  return HOOD_OK;
+  hood_error e;
+  return decode_error(c0, &e);
 }
 
 }  // namespace
@@ -617,10 +686,18 @@ int hood_merge_records(hood_ctx* ctx, const double* d_recs, int64_t G, int64_t c
 }
 
 int hood_merge_round_f32(hood_ctx* ctx, const float* d_in, int64_t n, int64_t d, float* d_out, void* stream) {
-  return merge_round<float>(ctx, d_in, n, d, d_out, reinterpret_cast<cudaStream_t>(stream));
+  return merge_round<float>(ctx, d_in, n, d, d_out, nullptr, reinterpret_cast<cudaStream_t>(stream));
 }
 int hood_merge_round_f64(hood_ctx* ctx, const double* d_in, int64_t n, int64_t d, double* d_out, void* stream) {
-  return merge_round<double>(ctx, d_in, n, d, d_out, reinterpret_cast<cudaStream_t>(stream));
+  return merge_round<double>(ctx, d_in, n, d, d_out, nullptr, reinterpret_cast<cudaStream_t>(stream));
+}
+int hood_merge_round_scratch_f32(hood_ctx* ctx, const float* d_in, int64_t n, int64_t d, float* d_out,
+                                 int32_t* d_scratch, void* stream) {
+  return merge_round<float>(ctx, d_in, n, d, d_out, d_scratch, reinterpret_cast<cudaStream_t>(stream));
+}
+int hood_merge_round_scratch_f64(hood_ctx* ctx, const double* d_in, int64_t n, int64_t d, double* d_out,
+                                 int32_t* d_scratch, void* stream) {
+  return merge_round<double>(ctx, d_in, n, d, d_out, d_scratch, reinterpret_cast<cudaStream_t>(stream));
 }
 
 // The round trace of build_hood (cli.cpp:163-166 observer + write_trace_round,
@@ -646,7 +723,7 @@ int hood_write_trace_f64(hood_ctx* ctx, const double* h_pts, int64_t n, const ch
     text.resize((size_t)len);
     hood_format_trace_round(h.data(), n, d, text.data(), len);
     if (std::fwrite(text.data(), 1, text.size(), f) != text.size()) rc = HOOD_ERR_INVALID_ARG;
-    if (rc == HOOD_OK) rc = merge_round<double>(ctx, d_a, n, d, d_b, 0);
+    if (rc == HOOD_OK) rc = merge_round<double>(ctx, d_a, n, d, d_b, nullptr, 0);
     if (rc == HOOD_OK && cudaMemcpy(h.data(), d_b, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) rc = HOOD_ERR_CUDA;
     std::swap(d_a, d_b);
   }
@@ -689,6 +766,8 @@ int hood_destroy(hood_ctx* c) {
   cudaFree(c->d_in);
   cudaFree(c->d_out);
   cudaFree(c->d_counts);
+  cudaFree(c->round_tmp);
+  if (c->order_ev) cudaEventDestroy(c->order_ev);
   if (c->s_copy) {
     for (auto& e : c->ev) cudaEventDestroy(e);
     cudaStreamDestroy(c->s_copy);

@@ -26,10 +26,21 @@
 #include "hood_device.cuh"
 #include "hood_kernels.cuh"
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 namespace hood_b200 {
+
+// In-kernel globaltimer / clock64 stamps (tools/trace_ring.py,
+// tools/trace_finalize.py): compiled in only with -DHOOD_TRACE, so the product
+// build carries none of it.
+#ifdef HOOD_TRACE
+constexpr bool kTrace = true;
+#else
+constexpr bool kTrace = false;
+#endif
 
 template <class S> struct HCap { static constexpr int value = 128; };  // running hood kept in smem (corners)
 
@@ -161,6 +172,8 @@ __global__ void err_reset_kernel(DevError* err, void* warm) {
   using V = typename PointT<S>::V;
   asm volatile("griddepcontrol.launch_dependents;");
   err->key = ~0ULL;
+  err->need = -1;
+  err->degen = ~0ULL;
   if (warm) {
     unsigned char* w = reinterpret_cast<unsigned char*>(warm);
     V* c = reinterpret_cast<V*>(w);
@@ -640,6 +653,99 @@ __device__ __noinline__ unsigned edge_survivors(unsigned a, long long q0, long l
   return svm;
 }
 
+// validate_points' collinearity margin over consecutive triples
+// (hoodbuf.cpp:16-26 check_triple, :59 the i, i+1, i+2 loop; hoodbuf.hpp:16
+// kCollinearMargin = 1e-9): |orient(p_k, p_i, p_j)| < 1e-9 for
+// (i, j, k) = (q-2, q-1, q) is an error at i.  The reference's double
+// expression, operand order kept, no FMA (floats widen exactly).  Only with
+// HOOD_FLAG_CHECK_TRIPLES; out of line so the hot kernel's registers do not
+// pay for it.
+__device__ __forceinline__ bool triple_degenerate(double ix, double iy, double jx, double jy, double kx, double ky) {
+  const double det = __dsub_rn(__dmul_rn(__dsub_rn(jx, ix), __dsub_rn(ky, iy)),
+                               __dmul_rn(__dsub_rn(jy, iy), __dsub_rn(kx, ix)));
+  return fabs(det) < 1e-9;
+}
+
+// Ring kernel: the lane's run (smem address a, first global index q0) inside
+// instance [ibase, lim).  The two points before the run are lane-1's last
+// two, or (lane 0) read from global memory.
+template <class S, int U>
+__device__ __noinline__ void triple_check_block(unsigned a, const typename PointT<S>::V* gpts, long long q0,
+                                                long long ibase, long long lim, DevError* err) {
+  using L = typename Ld16<S>::T;
+  constexpr int PPL = Ld16<S>::PPL, NP = U * PPL;
+  const int lane = threadIdx.x & 31;
+  double px[NP], py[NP];
+#pragma unroll
+  for (int k = 0; k < U; ++k) {
+    const L c = lds16<L>(a ^ (k << 4));
+#pragma unroll
+    for (int e = 0; e < PPL; ++e) {
+      px[k * PPL + e] = (double)pt_of(c, e).x;
+      py[k * PPL + e] = (double)pt_of(c, e).y;
+    }
+  }
+  double ax = __shfl_up_sync(0xffffffffu, px[NP - 2], 1), ay = __shfl_up_sync(0xffffffffu, py[NP - 2], 1);
+  double bx = __shfl_up_sync(0xffffffffu, px[NP - 1], 1), by = __shfl_up_sync(0xffffffffu, py[NP - 1], 1);
+  if (lane == 0) {
+    if (q0 - 2 >= ibase) {
+      ax = (double)gpts[q0 - 2].x;
+      ay = (double)gpts[q0 - 2].y;
+    }
+    if (q0 - 1 >= ibase) {
+      bx = (double)gpts[q0 - 1].x;
+      by = (double)gpts[q0 - 1].y;
+    }
+  }
+  unsigned long long bad = ~0ULL;
+#pragma unroll
+  for (int t = 0; t < NP; ++t) {
+    const long long q = q0 + t;
+    if (q < lim && q - 2 >= ibase && triple_degenerate(ax, ay, bx, by, px[t], py[t]))
+      bad = min(bad, kTripleKey + (unsigned long long)(q - 2));
+    ax = bx;
+    ay = by;
+    bx = px[t];
+    by = py[t];
+  }
+  if (bad != ~0ULL) {
+    err_ready();
+    atomicMin(&err->key, bad);
+  }
+}
+
+// Instance kernel: the thread's chunk v[0..nv) of global index base; its two
+// predecessors are in the same tile whenever they are in the same instance
+// (instances never straddle tiles).
+template <class S>
+__device__ __noinline__ void triple_check_chunk(const typename PointT<S>::V* v, int nv, const unsigned char* tile,
+                                                int t, long long base, long long L, DevError* err) {
+  constexpr int K = PointT<S>::K;
+  const TileAcc<S> X{const_cast<unsigned char*>(tile)};
+  const long long ibase = base & ~(L - 1);
+  double ax = 0, ay = 0, bx = 0, by = 0;
+  if (base - 2 >= ibase) {
+    ax = (double)X.ld((long long)t * K - 2).x;
+    ay = (double)X.ld((long long)t * K - 2).y;
+  }
+  if (base - 1 >= ibase) {
+    bx = (double)X.ld((long long)t * K - 1).x;
+    by = (double)X.ld((long long)t * K - 1).y;
+  }
+  unsigned long long bad = ~0ULL;
+  for (int i = 0; i < nv; ++i) {
+    const long long q = base + i;
+    const double cx = (double)v[i].x, cy = (double)v[i].y;
+    if (q - 2 >= ibase && triple_degenerate(ax, ay, bx, by, cx, cy))
+      bad = min(bad, kTripleKey + (unsigned long long)(q - 2));
+    ax = bx;
+    ay = by;
+    bx = cx;
+    by = cy;
+  }
+  if (bad != ~0ULL) atomicMin(&err->key, bad);
+}
+
 #ifndef HOOD_RING_WARPS
 #define HOOD_RING_WARPS 4
 #endif
@@ -699,7 +805,10 @@ __device__ __forceinline__ int ring_rot(int l) {
 // Every warp touches only its own smem, so no CTA barrier is ever needed.
 // LEAN: batched builds (units = whole instances, never a huge hood per unit)
 // use the register-light merge, 128 registers and 4 CTAs/SM.
-template <class S, int D, int P, int U_, bool LEAN = false>
+// TRI: the variant with validate_points' consecutive-triple margin check
+// fused into the landing pass (HOOD_FLAG_CHECK_TRIPLES builds only; a call in
+// the landing pass costs the plain kernel registers, so it is compiled apart).
+template <class S, int D, int P, int U_, bool LEAN = false, bool TRI = false>
 __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams<S> p) {
   using V = typename PointT<S>::V;
   using L = typename Ld16<S>::T;
@@ -850,6 +959,10 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
         }
       if (__any_sync(FULL, !in)) report(b, true);
     }
+    if constexpr (TRI) {
+      const long long ib = (long long)(b / bpi) * p.L;
+      triple_check_block<S, U>(a, gpts, (long long)b * BP + lane * NP, ib, min(n, ib + p.L), p.err);
+    }
     xc = __shfl_sync(FULL, xl, 31);
     if (__any_sync(FULL, !ok)) report(b, false);
     return fmax(m0, m1);
@@ -859,8 +972,8 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
   asm volatile("griddepcontrol.launch_dependents;");
   // profiling (p.trace, globaltimer ns): [0] first warp entry, [1] last warp
   // exit, [2] last prologue end; per warp gw at [1024 + 4 gw]: entry, exit, SM
-  if (p.trace && lane == 0) atomicMin(reinterpret_cast<unsigned long long*>(p.trace), gtimer());
-  if (p.trace && lane == 0) p.trace[1024 + 4 * gw] = (long long)gtimer();
+  if (kTrace && p.trace && lane == 0) atomicMin(reinterpret_cast<unsigned long long*>(p.trace), gtimer());
+  if (kTrace && p.trace && lane == 0) p.trace[1024 + 4 * gw] = (long long)gtimer();
 #ifdef HOOD_RING_COUNTERS
   int n_cand = 0, n_edge = 0, n_many = 0;
   long long c_cand = 0, c_flush = 0, c_land = 0;
@@ -951,7 +1064,7 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
   for (int i = 0; i + 1 < D; ++i) land_next(i + 1, lmw[i], win[i]);
   lmw[D - 1] = NEG;
   win[D - 1] = NEG;
-  if (p.trace && lane == 0) {
+  if (kTrace && p.trace && lane == 0) {
     const unsigned long long t = gtimer();
     atomicMax(reinterpret_cast<unsigned long long*>(p.trace) + 2, t);
 #ifndef HOOD_RING_COUNTERS
@@ -1194,8 +1307,8 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
     advance(cc);
   }
   cp_async_wait<0>();
-  if (p.trace && lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(p.trace) + 1, gtimer());
-  if (p.trace && lane == 0) {
+  if (kTrace && p.trace && lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(p.trace) + 1, gtimer());
+  if (kTrace && p.trace && lane == 0) {
     p.trace[1024 + 4 * gw + 1] = (long long)gtimer();
     unsigned smid;
     asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
@@ -1292,6 +1405,7 @@ instance_hull_kernel(const __grid_constant__ CUtensorMap tmap, const SlabParams<
         const bool inst_start = (base_pt & (p.L - 1)) == 0;  // L is a power of two here
         const S prevx = inst_start ? (S)0 : X.ld((long long)tid * K - 1).x;
         check_chunk<S>(v, nv, prevx, !inst_start, base_pt, p.check_range, p.err, gpts);
+        if (p.check_triples) triple_check_chunk<S>(v, nv, tile, tid, base_pt, p.L, p.err);
       }
 
       // exact segmented exclusive prefix / suffix max of chunk maxima
@@ -1572,7 +1686,7 @@ __device__ __noinline__ void finalize_body(const FinalizeParams<S> p) {
   double2* stg = reinterpret_cast<double2*>(smem_raw + o_stg);      // [MAXC][CAP]
   V* F = reinterpret_cast<V*>(smem_raw + o_stg + (size_t)MAXC * CAP * sizeof(double2));  // [2][fcap]
 
-  if (p.trace && threadIdx.x == 0) p.trace[29] = (long long)gtimer();  // resident
+  if (kTrace && p.trace && threadIdx.x == 0) p.trace[29] = (long long)gtimer();  // resident
   if (p.dry) {
     // the warm-up instance: no waits
   } else if (p.arrive) {
@@ -1592,7 +1706,7 @@ __device__ __noinline__ void finalize_body(const FinalizeParams<S> p) {
     asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the slab kernel has completed
   }
   if (p.done && *p.done) return;  // merged already (small exchange)
-  if (p.trace && tid == 0) {
+  if (kTrace && p.trace && tid == 0) {
     p.trace[0] = clock64();
     p.trace[30] = (long long)gtimer();
   }
@@ -1621,7 +1735,7 @@ __device__ __noinline__ void finalize_body(const FinalizeParams<S> p) {
 #pragma unroll
   for (int j = 0; j < R; ++j)
     if (ap[j].y > tbest.y) tbest = ap[j];
-  if (p.trace && tid == 0) p.trace[1] = clock64();
+  if (kTrace && p.trace && tid == 0) p.trace[1] = clock64();
   V pre_t, suf_t;
   block_excl_argmax2<V, NWP>(tbest, NOPT, shV, pre_t, suf_t);
 
@@ -1645,7 +1759,7 @@ __device__ __noinline__ void finalize_body(const FinalizeParams<S> p) {
   }
   int C;
   int cpos = block_excl_sum<NWP, false>(ncand, shI, &C);  // next shI use follows a barrier
-  if (p.trace && tid == 0) p.trace[2] = clock64();
+  if (kTrace && p.trace && tid == 0) p.trace[2] = clock64();
 
   if (C <= MAXC) {
 #pragma unroll
@@ -1693,7 +1807,7 @@ __device__ __noinline__ void finalize_body(const FinalizeParams<S> p) {
       }
     }
     __syncthreads();
-    if (p.trace && tid == 0) p.trace[3] = clock64();
+    if (kTrace && p.trace && tid == 0) p.trace[3] = clock64();
     static_assert(CAP == 32, "one lane per staged corner");
     if (C <= 32) {
       // the common case, without another CTA barrier: every warp reads the
@@ -1712,7 +1826,7 @@ __device__ __noinline__ void finalize_body(const FinalizeParams<S> p) {
       const int A = __shfl_sync(0xffffffffu, incl, 31);
       if (!__any_sync(0xffffffffu, mine > CAP) && A <= 64) {
         if (warp != 0) return;
-        if (p.trace && lane == 0) p.trace[4] = clock64();
+        if (kTrace && p.trace && lane == 0) p.trace[4] = clock64();
         const int off = incl - m;  // first survivor of candidate `lane`
         double2* Hd = reinterpret_cast<double2*>(F);
 #pragma unroll
@@ -1731,13 +1845,13 @@ __device__ __noinline__ void finalize_body(const FinalizeParams<S> p) {
           if (i < A) Hd[i] = stg[c * CAP + (i - oc)];
         }
         __syncwarp();
-        if (p.trace && lane == 0) p.trace[10] = clock64();
+        if (kTrace && p.trace && lane == 0) p.trace[10] = clock64();
         const int h = A ? warp_hull_small<double2>(Hd, A, Hd) : 0;
-        if (p.trace && lane == 0) p.trace[11] = p.trace[5] = clock64();
+        if (kTrace && p.trace && lane == 0) p.trace[11] = p.trace[5] = clock64();
         for (int e = lane; e < h; e += 32) gout[ibase + e] = make_vec<V>((S)Hd[e].x, (S)Hd[e].y);
         if (lane == 0) {
           p.out_counts[blockIdx.x] = h;
-          if (p.trace) {
+          if (kTrace && p.trace) {
             p.trace[6] = p.trace[7] = clock64();
             p.trace[8] = A;
             p.trace[9] = C;
@@ -1756,7 +1870,7 @@ __device__ __noinline__ void finalize_body(const FinalizeParams<S> p) {
     if (!ovf) {
       long long* rns = nsd;  // reuse the tree-node arrays: hull start / size
       int* rnc = ncd;
-      if (p.trace && tid == 0) p.trace[4] = clock64();
+      if (kTrace && p.trace && tid == 0) p.trace[4] = clock64();
       // the staged runs in x order (candidate order), widened to double
       // (exact): up to 64 survivors are hulled by one warp with iterated
       // pruning (a few rounds of parallel predicates, tools/micro/prune.cu);
@@ -1772,16 +1886,16 @@ __device__ __noinline__ void finalize_body(const FinalizeParams<S> p) {
           if (lane < min(cn[c], CAP)) Hd[cc[c] + lane] = stg[c * CAP + lane];
         __syncthreads();
         if (warp == 0) {
-          if (p.trace && lane == 0) p.trace[10] = clock64();
+          if (kTrace && p.trace && lane == 0) p.trace[10] = clock64();
           const int h = A ? warp_hull_small<double2>(Hd, A, Hd) : 0;
           if (lane == 0) {
             rns[0] = 0;
             rnc[0] = h;
-            if (p.trace) p.trace[11] = clock64();
+            if (kTrace && p.trace) p.trace[11] = clock64();
           }
         }
       } else if (tid == 0) {
-        if (p.trace) p.trace[10] = clock64();
+        if (kTrace && p.trace) p.trace[10] = clock64();
         int h = 0;
         double2 h1 = make_double2(0, 0), h2 = h1;
         for (int c = 0; c < C; ++c) {
@@ -1802,14 +1916,14 @@ __device__ __noinline__ void finalize_body(const FinalizeParams<S> p) {
         }
         rns[0] = 0;
         rnc[0] = h;
-        if (p.trace) p.trace[11] = clock64();
+        if (kTrace && p.trace) p.trace[11] = clock64();
       }
       __syncthreads();
-      if (p.trace && tid == 0) p.trace[5] = clock64();
+      if (kTrace && p.trace && tid == 0) p.trace[5] = clock64();
       const int n = rnc[0];
       for (int e = tid; e < n; e += kFinThreads) gout[ibase + e] = make_vec<V>((S)Hd[e].x, (S)Hd[e].y);
       if (tid == 0) p.out_counts[blockIdx.x] = n;
-      if (p.trace && tid == 0) {
+      if (kTrace && p.trace && tid == 0) {
         p.trace[6] = clock64();
         p.trace[7] = clock64();
         p.trace[8] = A;
@@ -1847,7 +1961,7 @@ __device__ __noinline__ void finalize_body(const FinalizeParams<S> p) {
     }
   }
   __syncthreads();
-  if (p.trace && tid == 0) p.trace[20] = clock64();
+  if (kTrace && p.trace && tid == 0) p.trace[20] = clock64();
   // concatenation fast path (arc-like slabs): when every slab kept a run and
   // every junction is convex -- the triples the monotone chain would test at
   // the seams, all strictly left -- the hood is the runs in order
@@ -1906,13 +2020,13 @@ __device__ __noinline__ void finalize_body(const FinalizeParams<S> p) {
   }
   if (ok) {
     if (tid == 0) p.out_counts[blockIdx.x] = tot;
-    if (p.trace && tid == 0) p.trace[21] = clock64();
+    if (kTrace && p.trace && tid == 0) p.trace[21] = clock64();
     return;
   }
   int levels = 0;
   while ((1 << levels) < M) ++levels;
   tree_merge<V>(PtrAcc<V>{gout}, nsd, ncd, M, levels);
-  if (p.trace && tid == 0) p.trace[21] = clock64();
+  if (kTrace && p.trace && tid == 0) p.trace[21] = clock64();
   // the merged hood to the instance's first slots: a forward copy in chunks
   // (every chunk is read before it is written, destination below source)
   const long long st = nsd[0];
@@ -2027,13 +2141,92 @@ void launch_block_count(const void* slots, long long n, long long d, int* counts
   block_count_kernel<S><<<(int)blocks, 256, 0, st>>>(reinterpret_cast<const V*>(slots), n, d, counts);
 }
 
+// One round of the reference loop (driver.cpp:20-43 + match_and_merge_kernel,
+// kernel.cpp:20-137) for the per-round seam hood_merge_round.  Pair b (window
+// [start, start+2d), start = 2bd) holds P = the m corners at start and Q = the
+// k corners at start+d.  One thread per pair finds the common tangent with
+// bridge() (the g/f classifiers as monotone searches) -- the (pindex, qindex)
+// the pinpoint phase leaves in scratch[start], scratch[start+1]
+// (kernel.cpp:101-112, absolute slots) -- and checks that it is unique: a
+// corner next to either end lying exactly on the bridge line (the reference's
+// double predicate) is the configuration in which no single (i, j) pair has
+// both classifiers EQUAL, i.e. DegenerateTangent (kernel.cpp:163-187) or the
+// pinpoint's write-write conflict (test_kernel.cpp:330-350); the first such
+// block goes to err->degen.
+template <class S>
+__global__ void round_seam_kernel(const typename PointT<S>::V* in, long long pairs, long long d, const int* counts,
+                                  int2* pq, int* scratch, DevError* err) {
+  using V = typename PointT<S>::V;
+  for (long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x; b < pairs;
+       b += (long long)gridDim.x * blockDim.x) {
+    const long long start = 2 * b * d;
+    const long long m = counts[2 * b], k = counts[2 * b + 1];
+    long long pi = -1, qi = -1;
+    if (m > 0 && k > 0) {
+      const PtrAcc<V> X{const_cast<V*>(in)};
+      bridge<V>(X, start, m, X, start + d, k, pi, qi);
+      const V p = in[start + pi], q = in[start + d + qi];
+      bool degen = false;
+      if (pi > 0) degen |= orient_sign(in[start + pi - 1], p, q) == 0;
+      if (pi + 1 < m) degen |= orient_sign(p, in[start + pi + 1], q) == 0;
+      if (qi > 0) degen |= orient_sign(p, in[start + d + qi - 1], q) == 0;
+      if (qi + 1 < k) degen |= orient_sign(p, q, in[start + d + qi + 1]) == 0;
+      if (degen) atomicMin(&err->degen, (unsigned long long)b);
+    } else if (k > 0) {  // an empty half: the other passes through whole
+      qi = 0;
+    } else if (m > 0) {
+      pi = m - 1;
+    }
+    pq[b] = make_int2((int)pi, (int)qi);
+    if (scratch) {
+      scratch[start] = (int)(start + pi);
+      scratch[start + 1] = (int)(start + d + qi);
+    }
+  }
+}
+
+// The splice (kernel.cpp:117-137): window slot o of pair b receives P[o] for
+// o <= pindex, then Q[qindex + (o - pindex - 1)], then REMOTE (10, 0).
+template <class S>
+__global__ void round_splice_kernel(const typename PointT<S>::V* in, long long n, long long d, const int* counts,
+                                    const int2* pq, typename PointT<S>::V* out) {
+  using V = typename PointT<S>::V;
+  const V remote{(S)10, (S)0};  // geom.hpp:14
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long b = i / (2 * d), start = 2 * b * d, o = i - start;
+    const int2 t = pq[b];
+    const long long k = counts[2 * b + 1];
+    const long long keep = t.x + 1, tail = t.y >= 0 ? k - t.y : 0;
+    V v = remote;
+    if (o < keep) v = in[start + o];
+    else if (o < keep + tail) v = in[start + d + t.y + (o - keep)];
+    out[i] = v;
+  }
+}
+
+template <class S>
+void launch_round_merge(const void* in, long long n, long long d, const int* counts, int* pq, int* scratch,
+                        void* out, DevError* err, cudaStream_t st) {
+  using V = typename PointT<S>::V;
+  const long long pairs = n / (2 * d);
+  const long long g1 = std::min((pairs + 127) / 128, 148LL * 16);
+  round_seam_kernel<S><<<(int)g1, 128, 0, st>>>(reinterpret_cast<const V*>(in), pairs, d, counts,
+                                                reinterpret_cast<int2*>(pq), scratch, err);
+  const long long g2 = std::min((n + 255) / 256, 148LL * 16);
+  round_splice_kernel<S><<<(int)g2, 256, 0, st>>>(reinterpret_cast<const V*>(in), n, d, counts,
+                                                  reinterpret_cast<const int2*>(pq), reinterpret_cast<V*>(out));
+}
+
 // Exchange record of one rank's slab hood: header (count, 0),
 // then the corners widened to double with x shifted into global coordinates.
 template <class S>
 __global__ void pack_record_kernel(const typename PointT<S>::V* corners, const int* count, long long cap,
-                                   double x_offset, double2* rec) {
+                                   double x_offset, double2* rec, DevError* err) {
   const long long k = min((long long)*count, cap);
-  if (blockIdx.x == 0 && threadIdx.x == 0) rec[0] = make_double2((double)*count, 0.0);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    rec[0] = make_double2((double)*count, 0.0);
+    if (*count > cap) atomicMax(&err->need, (long long)*count);  // never a silent truncation
+  }
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += (long long)gridDim.x * blockDim.x) {
     const typename PointT<S>::V c = corners[i];
     rec[1 + i] = make_double2((double)c.x + x_offset, (double)c.y);
@@ -2042,10 +2235,10 @@ __global__ void pack_record_kernel(const typename PointT<S>::V* corners, const i
 
 template <class S>
 void launch_pack_record(const void* corners, const int* count, long long cap, double x_offset, double* rec,
-                        cudaStream_t st) {
+                        DevError* err, cudaStream_t st) {
   using V = typename PointT<S>::V;
   pack_record_kernel<S><<<8, 256, 0, st>>>(reinterpret_cast<const V*>(corners), count, cap, x_offset,
-                                            reinterpret_cast<double2*>(rec));
+                                            reinterpret_cast<double2*>(rec), err);
 }
 
 // G gathered records -> the global hood, by one CTA when the exchange is
@@ -2058,7 +2251,8 @@ void launch_pack_record(const void* corners, const int* count, long long cap, do
 // hulled by one warp when at most 64 remain.  *done tells the following
 // finalize whether the result is already written.
 __global__ void __launch_bounds__(256) gather_records_kernel(const double2* recs, long long G, long long cap,
-                                                             double2* out, int* seg_cnt, int* out_count, int* done) {
+                                                             double2* out, int* seg_cnt, int* out_count, int* done,
+                                                             DevError* err) {
   asm volatile("griddepcontrol.launch_dependents;");
   constexpr int GM = 256, NWP = 8;
   __shared__ double2 stage[64];
@@ -2068,6 +2262,12 @@ __global__ void __launch_bounds__(256) gather_records_kernel(const double2* recs
   const double NEG = neg_inf<double>();
   const double2 NOPT = make_double2(NEG, NEG);
   const bool small = G <= GM;
+  // a header count above cap: that slab hood was truncated by its pack --
+  // reported (err->need), never merged silently as if complete
+  for (long long g = tid; g < G; g += blockDim.x) {
+    const long long c = (long long)recs[g * (cap + 1)].x;
+    if (c > cap) atomicMax(&err->need, c);
+  }
   if (small && tid < G) {
     const int c = (int)recs[(long long)tid * (cap + 1)].x;
     cnt_s[tid] = c < cap ? c : (int)cap;
@@ -2179,59 +2379,72 @@ __global__ void __launch_bounds__(256) gather_records_kernel(const double2* recs
 }
 
 void launch_gather_records(const double* recs, long long G, long long cap, double* out, int* seg_cnt,
-                           int* out_count, int* done, cudaStream_t st) {
+                           int* out_count, int* done, DevError* err, cudaStream_t st) {
   gather_records_kernel<<<1, 256, 0, st>>>(reinterpret_cast<const double2*>(recs), G, cap,
-                                            reinterpret_cast<double2*>(out), seg_cnt, out_count, done);
+                                            reinterpret_cast<double2*>(out), seg_cnt, out_count, done, err);
 }
 
 // ------------------------------------------------------------------ host side
 
-// Ring kernel shape: D blocks of lookahead, P blocks in flight per warp, U
-// 16-byte chunks per lane per block (blocks of 2 KB for U = 4, 4 KB for
-// U = 8); selected once per process (HOOD_RING=<D><P><U>, e.g. 234, overrides
-// it for experiments).
-#define HOOD_RING_SHAPES(X) X(1, 1, 8) X(1, 2, 8) X(2, 2, 8) X(2, 3, 4)
-// measured best (B200, round 1): (1, 1, 8) for both storages -- one block of
-// lookahead, one in flight, 4 KB blocks (tools/gpu_sweep.sh)
-template <class S>
-constexpr int kRingDefault = 118;
-template <class S>
-static int ring_shape() {
-  static int d = [] {
-    int v = kRingDefault<S>;
-    if (const char* e = std::getenv("HOOD_RING")) v = std::atoi(e);
-#define HOOD_RING_OK(D, P, U) if (v == D * 100 + P * 10 + U) return v;
-    HOOD_RING_SHAPES(HOOD_RING_OK)
-#undef HOOD_RING_OK
-    return kRingDefault<S>;
-  }();
-  return d;
-}
+// Ring kernel shape: D = 1 block of lookahead, P = 1 block in flight per
+// warp, U = 8 16-byte chunks per lane per block (4 KB blocks).  Measured best
+// of (1,1,8), (1,2,8), (2,2,8), (2,3,4) on B200 for both storages (round 1,
+// tools/gpu_sweep.sh); the other shapes are no longer compiled.
+constexpr int kRingD = 1, kRingP = 1, kRingU = 8;
 
-template <class S, int D, int P, int U>
+template <class S, bool LEAN>
 static size_t ring_smem() {
-  return (size_t)kRingWarps * RingLayout<S, D, P, U>::BYTES + 128;  // + alignment pad
+  return (size_t)kRingWarps * RingLayout<S, kRingD, kRingP, kRingU>::BYTES + 128;  // + alignment pad
 }
 
-template <class S, int D, int P, int U, bool LEAN = false>
-static int ring_occ_of() {
-  const size_t smem = ring_smem<S, D, P, U>();
-  cudaFuncSetAttribute(ring_hull_kernel<S, D, P, U, LEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int o = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ring_hull_kernel<S, D, P, U, LEAN>, 32 * kRingWarps, smem);
-  return o > 0 ? o : 1;
+// Per-device launch state: the dynamic shared-memory opt-in
+// (cudaFuncAttributeMaxDynamicSharedMemorySize) is a per-device attribute, so
+// it is set -- and the occupancy read -- once for every device a process
+// builds on, not once per process.
+constexpr int kMaxDevices = 64;
+struct DevLaunchState {
+  int ring_occ = 0, ring_occ_lean = 0, inst_occ = 0;  // the TRI variants run at the same occupancy or less
+  bool fin_attr = false;
+};
+static DevLaunchState g_dev_state[kMaxDevices][2];  // [device][f64]
+static std::mutex g_dev_mu;
+
+template <class S>
+static const DevLaunchState& dev_state() {
+  int d = 0;
+  cudaGetDevice(&d);
+  if (d < 0 || d >= kMaxDevices) d = 0;
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  DevLaunchState& st = g_dev_state[d][sizeof(S) == 8];
+  if (st.ring_occ == 0) {
+    auto occ_of = [](auto kern, size_t smem, int threads) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int o = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem);
+      return o > 0 ? o : 1;
+    };
+    st.ring_occ_lean = occ_of(ring_hull_kernel<S, kRingD, kRingP, kRingU, true>, ring_smem<S, true>(),
+                              32 * kRingWarps);
+    st.inst_occ = occ_of(instance_hull_kernel<S>, inst_smem_bytes<S>(), kThreads);
+    occ_of(ring_hull_kernel<S, kRingD, kRingP, kRingU, true, true>, ring_smem<S, true>(), 32 * kRingWarps);
+    occ_of(ring_hull_kernel<S, kRingD, kRingP, kRingU, false, true>, ring_smem<S, false>(), 32 * kRingWarps);
+    cudaFuncSetAttribute(finalize_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    st.fin_attr = true;
+    st.ring_occ = occ_of(ring_hull_kernel<S, kRingD, kRingP, kRingU, false>, ring_smem<S, false>(),
+                         32 * kRingWarps);
+  }
+  return st;
 }
 
-// the lean variant exists for the default shape only
 template <class S>
 bool ring_lean_available() {
-  return ring_shape<S>() == kRingDefault<S>;
+  return true;
 }
 
 template <class S>
 int slab_tile_rows(bool hmode) {
   // hmode: points per ring block, in 128-byte chunk rows of K points
-  return hmode ? 32 * (ring_shape<S>() % 10) * Ld16<S>::PPL / PointT<S>::K : kThreads;
+  return hmode ? 32 * kRingU * Ld16<S>::PPL / PointT<S>::K : kThreads;
 }
 
 template <class S>
@@ -2241,49 +2454,26 @@ int slab_warps_per_cta() {
 
 template <class S>
 int slab_kernel_occupancy(bool lean) {
-  if (lean) {
-    static int occ_lean = -1;
-    if (occ_lean < 0) occ_lean = ring_occ_of<S, kRingDefault<S> / 100, (kRingDefault<S> / 10) % 10, kRingDefault<S> % 10,
-                                             true>();
-    return occ_lean;
-  }
-  static int occ = -1;
-  if (occ < 0) {
-    switch (ring_shape<S>()) {
-#define HOOD_RING_OCC(D, P, U) \
-  case D * 100 + P * 10 + U: occ = ring_occ_of<S, D, P, U>(); break;
-      HOOD_RING_SHAPES(HOOD_RING_OCC)
-#undef HOOD_RING_OCC
-    }
-  }
-  return occ;
+  const DevLaunchState& st = dev_state<S>();
+  return lean ? st.ring_occ_lean : st.ring_occ;
 }
 
 template <class S>
 int instance_kernel_occupancy() {
-  static int occ = -1;
-  if (occ < 0) {
-    cudaFuncSetAttribute(instance_hull_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)inst_smem_bytes<S>());
-    int o = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, instance_hull_kernel<S>, kThreads, inst_smem_bytes<S>());
-    occ = o > 0 ? o : 1;
-  }
-  return occ;
+  return dev_state<S>().inst_occ;
 }
 
 template <class S>
 void launch_slab_kernel(const SlabParams<S>& p, const CUtensorMap* tmap, int grid, cudaStream_t st, bool reset_err,
                         void* warm) {
+  dev_state<S>();
   if (!p.hmode) {
-    instance_kernel_occupancy<S>();
     instance_hull_kernel<S><<<grid, kThreads, inst_smem_bytes<S>(), st>>>(*tmap, p);
     return;
   }
   // reset_err: the error record is reset by a one-thread kernel ahead of the
   // ring kernel, which follows it as a programmatic dependent
   if (reset_err) err_reset_kernel<S><<<1, 1, 0, st>>>(p.err, warm);
-  slab_kernel_occupancy<S>(p.lean != 0);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(32 * kRingWarps);
@@ -2293,20 +2483,13 @@ void launch_slab_kernel(const SlabParams<S>& p, const CUtensorMap* tmap, int gri
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = reset_err ? 1 : 0;
-  if (p.lean) {
-    constexpr int D = kRingDefault<S> / 100, P = (kRingDefault<S> / 10) % 10, U = kRingDefault<S> % 10;
-    cfg.dynamicSmemBytes = ring_smem<S, D, P, U>();
-    cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, D, P, U, true>, p);
-    return;
-  }
-  switch (ring_shape<S>()) {
-#define HOOD_RING_LAUNCH(D, P, U)                        \
-  case D * 100 + P * 10 + U:                             \
-    cfg.dynamicSmemBytes = ring_smem<S, D, P, U>();      \
-    cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, D, P, U>, p); \
-    break;
-    HOOD_RING_SHAPES(HOOD_RING_LAUNCH)
-#undef HOOD_RING_LAUNCH
+  cfg.dynamicSmemBytes = p.lean ? ring_smem<S, true>() : ring_smem<S, false>();
+  if (p.check_triples) {
+    if (p.lean) cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kRingU, true, true>, p);
+    else cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kRingU, false, true>, p);
+  } else {
+    if (p.lean) cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kRingU, true, false>, p);
+    else cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kRingU, false, false>, p);
   }
 }
 
@@ -2321,11 +2504,7 @@ template <class S>
 void launch_finalize(const FinalizeParams<S>& p, int instances, cudaStream_t st, bool pdl) {
   using V = typename PointT<S>::V;
   const size_t bytes = finalize_smem(p.fcap * (int)sizeof(V), p.slabs_per_inst);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(finalize_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  dev_state<S>();  // the 227 KB opt-in on this device
   if (!pdl) {
     finalize_kernel<S><<<instances, kFinThreads, bytes, st>>>(p);
     return;
@@ -2361,10 +2540,16 @@ template void launch_slab_kernel<double>(const SlabParams<double>&, const CUtens
                                          void*);
 template void launch_finalize<float>(const FinalizeParams<float>&, int, cudaStream_t, bool);
 template void launch_finalize<double>(const FinalizeParams<double>&, int, cudaStream_t, bool);
-template void launch_pack_record<float>(const void*, const int*, long long, double, double*, cudaStream_t);
-template void launch_pack_record<double>(const void*, const int*, long long, double, double*, cudaStream_t);
+template void launch_pack_record<float>(const void*, const int*, long long, double, double*, DevError*,
+                                        cudaStream_t);
+template void launch_pack_record<double>(const void*, const int*, long long, double, double*, DevError*,
+                                         cudaStream_t);
 template void launch_block_count<float>(const void*, long long, long long, int*, cudaStream_t);
 template void launch_block_count<double>(const void*, long long, long long, int*, cudaStream_t);
+template void launch_round_merge<float>(const void*, long long, long long, const int*, int*, int*, void*, DevError*,
+                                        cudaStream_t);
+template void launch_round_merge<double>(const void*, long long, long long, const int*, int*, int*, void*,
+                                         DevError*, cudaStream_t);
 template void launch_pad_fill<float>(void*, const void*, const int*, long long, long long, cudaStream_t);
 template void launch_pad_fill<double>(void*, const void*, const int*, long long, long long, cudaStream_t);
 template int slab_kernel_occupancy<float>(bool);

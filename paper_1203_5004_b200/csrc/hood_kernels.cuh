@@ -23,10 +23,17 @@ constexpr int kMinUnitBlocks = HOOD_MIN_UNIT_BLOCKS;  // ring kernel: blocks per
 
 // First error of a build, encoded as key = index*2 + (x_not_increasing ? 1 : 0)
 // so one atomicMin keeps validate_points' order (hoodbuf.cpp:48-58: at the
-// same index the range check fires before the order check).
+// same index the range check fires before the order check); consecutive-triple
+// margin errors (hoodbuf.cpp:53-60, checked only after every x check) take
+// key = kTripleKey + i, above every x key.  `need` (max, -1 = none) is the
+// record capacity a multi-GPU exchange needed when a slab hood did not fit.
+// Reset: all bytes 0xff.
 struct DevError {
   unsigned long long key;
+  long long need;
+  unsigned long long degen;  // hood_merge_round: first block with a degenerate tangent (min, ~0 = none)
 };
+constexpr unsigned long long kTripleKey = 1ULL << 62;
 
 template <class S>
 struct SlabParams {
@@ -50,6 +57,7 @@ struct SlabParams {
   long long* seg_base;
   DevError* err;
   int check_range;          // also flag x outside (0,1) (validate_points)
+  int check_triples;        // also flag consecutive triples within the collinearity margin
   int dbg;                  // 0 normal; 1 stream only (profiling); 2 no merger work
   long long* trace;         // optional per-tile clock64 trace (profiling)
   long long read_lim;       // points at or past this index may not be read yet (host-path chunks)
@@ -96,14 +104,25 @@ void launch_pad_fill(void* padded, const void* corners, const int* counts, long 
                      cudaStream_t st);
 template <class S>
 void launch_block_count(const void* slots, long long n, long long d, int* counts, cudaStream_t st);
+// One reference round on REMOTE-padded blocks (kernel.cpp:20-137): per pair
+// of blocks the common tangent (pindex, qindex) by bridge() -- optionally left
+// in scratch[start], scratch[start+1] as the pinpoint phase does -- with a
+// degenerate tangent (another corner on the bridge line) reported in
+// err->degen; then the splice into out (out != in).
+template <class S>
+void launch_round_merge(const void* in, long long n, long long d, const int* counts, int* pq, int* scratch,
+                        void* out, DevError* err, cudaStream_t st);
 // Multi-GPU exchange records: [count, 0 | corners (double, x + x_offset)], cap corners each.
+// A slab hood of more than cap corners is reported in err->need (the record
+// then holds its first cap corners and the true count in its header).
 template <class S>
 void launch_pack_record(const void* corners, const int* count, long long cap, double x_offset, double* rec,
-                        cudaStream_t st);
+                        DevError* err, cudaStream_t st);
 // G records -> segments of stride cap in out (double2) + seg counts; hulls them directly
 // (done = 1) when at most 64 corners arrived in total.
+// A record whose header count exceeds cap is reported in err->need.
 void launch_gather_records(const double* recs, long long G, long long cap, double* out, int* seg_cnt,
-                           int* out_count, int* done, cudaStream_t st);
+                           int* out_count, int* done, DevError* err, cudaStream_t st);
 template <class S>
 int slab_kernel_occupancy(bool lean = false);  // ring-kernel CTAs per SM
 template <class S>

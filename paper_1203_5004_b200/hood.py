@@ -34,6 +34,7 @@ HOOD_ERR_NOT_POWER_OF_TWO = 7
 HOOD_ERR_PARSE = 8
 HOOD_ERR_DEGENERATE_TRIPLE = 9
 HOOD_FLAG_CHECK_RANGE = 0x1
+HOOD_FLAG_CHECK_TRIPLES = 0x2
 
 EXPORTS = [
     "hood_create", "hood_destroy", "hood_reserve", "hood_build_f32", "hood_build_f64",
@@ -44,6 +45,7 @@ EXPORTS = [
     "hood_format_section", "hood_format_trace_round", "hood_write_trace_f64",
     "hood_pack_record_f32", "hood_pack_record_f64", "hood_merge_records",
     "hood_build_multi_f32", "hood_build_multi_f64",
+    "hood_merge_round_scratch_f32", "hood_merge_round_scratch_f64",
 ]
 
 
@@ -90,6 +92,8 @@ def library():
                 getattr(L, nm).argtypes = [p, p, p, i64, i64, p, p, p]
             for nm in ("hood_merge_round_f32", "hood_merge_round_f64"):
                 getattr(L, nm).argtypes = [p, p, i64, i64, p, p]
+            for nm in ("hood_merge_round_scratch_f32", "hood_merge_round_scratch_f64"):
+                getattr(L, nm).argtypes = [p, p, i64, i64, p, p, p]
             for nm in ("hood_pack_record_f32", "hood_pack_record_f64"):
                 getattr(L, nm).argtypes = [p, p, p, i64, ctypes.c_double, p, p]
             L.hood_merge_records.argtypes = [p, p, i64, i64, p, p, p]
@@ -108,18 +112,30 @@ def library():
     return _lib
 
 
+class CapacityError(HoodError):
+    """A multi-GPU exchange record was too small: .index is the capacity needed."""
+
+
 def _raise(code: int, index: int = -1):
     msg = library().hood_status_string(code).decode()
     if code in (HOOD_ERR_X_NOT_INCREASING, HOOD_ERR_X_OUT_OF_RANGE, HOOD_ERR_NOT_POWER_OF_TWO,
                 HOOD_ERR_DEGENERATE_TRIPLE):
         raise ValidationError(code, f"point {index}: {msg}", index)
+    if code == HOOD_ERR_CAPACITY:
+        raise CapacityError(code, f"{msg}: {index} slots needed", index)
     raise HoodError(code, msg, index)
 
 
 class Context:
-    """One hood_ctx per device (hood_create / hood_destroy)."""
+    """One hood_ctx per (device, host thread) (hood_create / hood_destroy).
 
-    _per_device: dict = {}
+    A context's workspace is reused by every build it runs, so contexts are
+    never shared between threads (ctypes releases the GIL during the calls);
+    the C-ABI orders a build on another stream than the context's last one
+    after it (include/hood_b200.h)."""
+
+    _per_key: dict = {}
+    _key_lock = threading.Lock()
 
     def __init__(self, device: int = 0):
         L = library()
@@ -132,9 +148,11 @@ class Context:
 
     @classmethod
     def get(cls, device: int) -> "Context":
-        c = cls._per_device.get(device)
-        if c is None:
-            c = cls._per_device[device] = Context(device)
+        key = (device, threading.get_ident())
+        with cls._key_lock:
+            c = cls._per_key.get(key)
+            if c is None:
+                c = cls._per_key[key] = Context(device)
         return c
 
     def __del__(self):
@@ -195,8 +213,12 @@ def _check_points(points):
         raise TypeError("points must be contiguous")
 
 
+def _flags(check_range: bool, check_triples: bool) -> int:
+    return (HOOD_FLAG_CHECK_RANGE if check_range else 0) | (HOOD_FLAG_CHECK_TRIPLES if check_triples else 0)
+
+
 def build_hood_async(points, block_len: int = 0, corners=None, counts=None, padded=None,
-                     check_range: bool = False, stream=None) -> BuildReport:
+                     check_range: bool = False, stream=None, check_triples: bool = False) -> BuildReport:
     """Enqueue a build on `stream` (default: torch's current stream); no sync."""
     import torch
     _check_points(points)
@@ -214,17 +236,20 @@ def build_hood_async(points, block_len: int = 0, corners=None, counts=None, padd
     fn = library().hood_build_f64 if points.dtype == torch.float64 else library().hood_build_f32
     rc = fn(ctx.handle, points.data_ptr(), n, L, corners.data_ptr(), counts.data_ptr(),
             padded.data_ptr() if padded is not None else None,
-            HOOD_FLAG_CHECK_RANGE if check_range else 0, ctypes.c_void_p(stream.cuda_stream))
+            _flags(check_range, check_triples), ctypes.c_void_p(stream.cuda_stream))
     if rc:
         _raise(rc)
     return BuildReport(corners=corners, counts=counts, block_len=L, padded=padded)
 
 
-def build_hood(points, block_len: int = 0, padded: bool = False, check_range: bool = False) -> BuildReport:
-    """driver.cpp:19-45 drop-in: build, synchronize, raise ValidationError on bad input."""
+def build_hood(points, block_len: int = 0, padded: bool = False, check_range: bool = False,
+               check_triples: bool = False) -> BuildReport:
+    """driver.cpp:19-45 drop-in: build, synchronize, raise ValidationError on bad input
+    (check_range / check_triples add validate_points' x-range and consecutive-triple
+    margin checks, hoodbuf.cpp:30-60, fused into the build)."""
     import torch
     pad = torch.empty_like(points) if padded else None
-    rep = build_hood_async(points, block_len, padded=pad, check_range=check_range)
+    rep = build_hood_async(points, block_len, padded=pad, check_range=check_range, check_triples=check_triples)
     Context.get(points.device.index if points.device.index is not None else torch.cuda.current_device()).last_error()
     return rep
 
@@ -235,7 +260,8 @@ def upper_hull(points):
     return rep.hull
 
 
-def build_hood_host(points_np, block_len: int = 0, check_range: bool = False, device: int = 0):
+def build_hood_host(points_np, block_len: int = 0, check_range: bool = False, device: int = 0,
+                    check_triples: bool = False):
     """Host buffers in / out through hood_build_host_* (the e2e path).
     Returns (corners ndarray (n,2), counts ndarray)."""
     import numpy as np
@@ -249,7 +275,7 @@ def build_hood_host(points_np, block_len: int = 0, check_range: bool = False, de
     ctx = Context.get(device)
     fn = library().hood_build_host_f64 if a.dtype == np.float64 else library().hood_build_host_f32
     rc = fn(ctx.handle, a.ctypes.data, n, L, out.ctypes.data, counts.ctypes.data,
-            HOOD_FLAG_CHECK_RANGE if check_range else 0)
+            _flags(check_range, check_triples))
     if rc:
         e = _Err()
         library().hood_last_error(ctx.handle, ctypes.byref(e))
@@ -344,9 +370,13 @@ def build_multi(slabs, contexts=None, x_offsets=None, cap: int = 4096):
     return out[: int(cnt.item())]
 
 
-def merge_round(slots, d: int, out=None, stream=None):
+def merge_round(slots, d: int, out=None, stream=None, scratch=None):
     """One reference round on the GPU (driver.cpp:20-43, kernel.cpp:155-161):
-    slots (n, 2) in HoodBuffer layout with blocks of d -> blocks of 2d."""
+    slots (n, 2) in HoodBuffer layout with blocks of d -> blocks of 2d.
+    scratch: optional (n,) int32 CUDA tensor that receives the pinpoint
+    phase's pindex / qindex at every pair window's first two slots
+    (kernel.cpp:101-112).  Asynchronous: ctx.last_error() (or
+    merge_round_checked) reports a degenerate tangent."""
     import torch
     if not isinstance(slots, torch.Tensor) or not slots.is_cuda or slots.dim() != 2 or slots.shape[1] != 2:
         raise TypeError("slots must be a CUDA tensor of shape (n, 2)")
@@ -357,10 +387,30 @@ def merge_round(slots, d: int, out=None, stream=None):
         out = torch.empty_like(slots)
     if stream is None:
         stream = torch.cuda.current_stream(slots.device)
-    fn = library().hood_merge_round_f64 if slots.dtype == torch.float64 else library().hood_merge_round_f32
-    rc = fn(ctx.handle, slots.data_ptr(), slots.shape[0], int(d), out.data_ptr(), ctypes.c_void_p(stream.cuda_stream))
+    if scratch is None:
+        fn = library().hood_merge_round_f64 if slots.dtype == torch.float64 else library().hood_merge_round_f32
+        rc = fn(ctx.handle, slots.data_ptr(), slots.shape[0], int(d), out.data_ptr(),
+                ctypes.c_void_p(stream.cuda_stream))
+    else:
+        if scratch.dtype != torch.int32 or scratch.numel() < slots.shape[0] or not scratch.is_cuda:
+            raise TypeError("scratch must be an int32 CUDA tensor of n entries")
+        fn = (library().hood_merge_round_scratch_f64 if slots.dtype == torch.float64
+              else library().hood_merge_round_scratch_f32)
+        rc = fn(ctx.handle, slots.data_ptr(), slots.shape[0], int(d), out.data_ptr(), scratch.data_ptr(),
+                ctypes.c_void_p(stream.cuda_stream))
     if rc:
         _raise(rc)
+    return out
+
+
+def match_and_merge_block(slots, d: int, scratch=None):
+    """kernel.cpp:175-187 on the GPU: merge the pair windows of slots (blocks
+    of d), synchronize, raise HoodError(HOOD_ERR_DEGENERATE) (.index = the
+    block) where the reference throws DegenerateTangent."""
+    import torch
+    out = merge_round(slots, d, scratch=scratch)
+    dev = slots.device.index if slots.device.index is not None else torch.cuda.current_device()
+    Context.get(dev).last_error()
     return out
 
 

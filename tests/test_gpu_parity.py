@@ -629,3 +629,189 @@ def test_bare_read_reference_kernel_runs():
     torch.cuda.synchronize()
     assert rc == 0 and torch.equal(t, before)
     assert H.library().hood_internal_stream_read(ctx.handle, None, ctypes.c_longlong(64), None) != 0
+
+
+# ------------------------------------------------ round 2: seams and errors
+
+def test_merge_round_scratch_reference_pairs(golden):
+    """The pinpoint phase's scratch (kernel.cpp:101-112): after the round,
+    scratch[start] = pindex and scratch[start+1] = qindex, the values the
+    reference's match_and_merge_block leaves (test_kernel.cpp:302-328)."""
+    P = golden("pairs.npz")
+    for d in sorted(set(int(x) for x in P["pq"][:, 0])):
+        idx = [t for t in range(P["pq"].shape[0]) if int(P["pq"][t, 0]) == d]
+        buf = np.concatenate([P["slots"][t][: 2 * d] for t in idx])
+        sc = torch.full((buf.shape[0],), -7, dtype=torch.int32, device="cuda")
+        out = H.match_and_merge_block(torch.as_tensor(buf).cuda(), d, scratch=sc)
+        got = sc.cpu().numpy().reshape(len(idx), 2 * d)[:, :2]
+        want = np.stack([P["scratch01"][t] for t in idx]) + np.arange(len(idx))[:, None] * 2 * d
+        assert np.array_equal(got, want), d
+        assert same(out.cpu().numpy(), np.concatenate([P["merged"][t][: 2 * d] for t in idx])), d
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_merge_round_scratch_known_answers(dtype):
+    """E1 (test_kernel.cpp:98-102): pindex 1, qindex 2; singletons
+    (test_kernel.cpp:141-151): 0 and 2; stale corners (test_kernel.cpp:153-168)
+    with its tangent (0, 3) -> slots 0 and 7."""
+    cases = [([A, B, C, D], 2, (1, 2), [A, B, C, D]),
+             ([(0.2, 0.4), R, (0.6, 0.3), R], 2, (0, 2), [(0.2, 0.4), (0.6, 0.3), R, R]),
+             ([(0.05, 0.5), (0.1, 0.45), (0.15, 0.35), (0.2, 0.2),
+               (0.8, 0.2), (0.85, 0.35), (0.9, 0.45), (0.95, 0.5)], 4, (0, 7),
+              [(0.05, 0.5), (0.95, 0.5), R, R, R, R, R, R])]
+    for slots, d, pq, merged in cases:
+        t = torch.as_tensor(np.array(slots), dtype=dtype).cuda()
+        sc = torch.zeros(t.shape[0], dtype=torch.int32, device="cuda")
+        out = H.match_and_merge_block(t, d, scratch=sc)
+        assert tuple(sc[:2].cpu().tolist()) == pq
+        assert same(out.cpu().numpy(), np.array(merged, dtype=np.float64).astype(out.cpu().numpy().dtype))
+
+
+def test_merge_round_flags_degenerate_tangent():
+    """test_kernel.cpp:330-350: p2, p3 and q1 on one dyadic line -- the
+    reference flags the block (DegenerateTangent or a pinpoint write-write
+    conflict); hood_merge_round reports HOOD_ERR_DEGENERATE for block 0, and a
+    clean pair next to it does not mask it."""
+    deg = [(0.0625, 0.25), (0.125, 0.4), (0.25, 0.5), (0.3125, 0.46875),
+           (0.5625, 0.3), (0.625, 0.3125), (0.6875, 0.28), (0.75, 0.2)]
+    ok = [(0.1, 0.5), (0.2, 0.6), (0.6, 0.9), (0.7, 0.2), (0.75, 0.1), (0.8, 0.15), (0.85, 0.12), (0.9, 0.05)]
+    for blocks, bad in [([deg], 0), ([ok, deg], 1), ([deg, ok], 0)]:
+        t = torch.as_tensor(np.concatenate([np.array(b) for b in blocks])).cuda()
+        with pytest.raises(H.HoodError) as ei:
+            H.match_and_merge_block(t, 4)
+        assert ei.value.code == H.HOOD_ERR_DEGENERATE and ei.value.index == bad
+    H.match_and_merge_block(torch.as_tensor(np.array(ok)).cuda(), 4)  # clean: no error
+
+
+def _triple_points(n, bad_i, seed):
+    """x strictly increasing on the 2^-24 grid, y random; with bad_i >= 0 the
+    triple (bad_i, bad_i+1, bad_i+2) is made exactly collinear."""
+    rng = np.random.default_rng(seed)
+    x = (np.arange(n) * 8 + rng.integers(1, 8, size=n)) * 2.0 ** -24 * (1 << 20) / n
+    y = rng.integers(1 << 20, 1 << 23, size=n) * 2.0 ** -24
+    if bad_i >= 0:
+        y[bad_i + 2] = y[bad_i] + (y[bad_i + 1] - y[bad_i]) * (x[bad_i + 2] - x[bad_i]) / (x[bad_i + 1] - x[bad_i])
+    return np.stack([x, y], axis=1)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_check_triples_first_index(oracle_mod, dtype):
+    """HOOD_FLAG_CHECK_TRIPLES: validate_points' consecutive-triple margin
+    (hoodbuf.cpp:16-26, :59) fused into the build: the first degenerate i is
+    reported, exactly the reference's double |orient| < 1e-9 on the stored
+    values, and x errors win over triple errors (hoodbuf.cpp:48-58 first)."""
+    import ctypes
+    L = H.library()
+    for n, bad in [(1 << 16, 40000), (1 << 16, 1), (1 << 20, 777777), (5000, 4097), (3000, 0)]:
+        p = _triple_points(n, bad, seed=n + bad)
+        t = torch.as_tensor(p, dtype=dtype).cuda()
+        stored = t.double().cpu().numpy()
+        xs, ys = stored[:, 0], stored[:, 1]
+        det = (xs[1:-1] - xs[:-2]) * (ys[2:] - ys[:-2]) - (ys[1:-1] - ys[:-2]) * (xs[2:] - xs[:-2])
+        first = int(np.nonzero(np.abs(det) < 1e-9)[0][0]) if np.any(np.abs(det) < 1e-9) else -1
+        assert first >= 0
+        with pytest.raises(H.ValidationError) as ei:
+            H.build_hood(t, check_triples=True)
+        assert ei.value.code == H.HOOD_ERR_DEGENERATE_TRIPLE and ei.value.index == first, (n, bad)
+        # the host path and the reference validate_points agree on the index
+        if O_ref_ok(oracle_mod) and dtype == torch.float64:
+            r = oracle_mod.ref_validate_points(stored)
+            if r != -1 and r[1][1] == r[1][0] + 1 and r[1][2] == r[1][0] + 2 and n > 64 and n & (n - 1) == 0:
+                assert r[1][0] == first
+        # without the flag the same points build fine (and match the oracle)
+        assert same(H.build_hood(t).hull.cpu().numpy(), oracle_mod.upper_hull(stored))
+    # an x error before the triple wins
+    p = _triple_points(1 << 14, 100, seed=3)
+    p[9000, 0] = p[8999, 0]
+    with pytest.raises(H.ValidationError) as ei:
+        H.build_hood(torch.as_tensor(p).cuda(), check_triples=True)
+    assert ei.value.code == H.HOOD_ERR_X_NOT_INCREASING and ei.value.index == 9000
+    # clean input passes with the flag on; batched instances never cross
+    p = np.concatenate([_triple_points(1024, -1, seed=s) for s in range(64)])
+    t = torch.as_tensor(p).cuda()
+    stored = p
+    ok = True
+    for i in range(64):
+        q = stored[i * 1024:(i + 1) * 1024]
+        det = (q[1:-1, 0] - q[:-2, 0]) * (q[2:, 1] - q[:-2, 1]) - (q[1:-1, 1] - q[:-2, 1]) * (q[2:, 0] - q[:-2, 0])
+        ok &= not np.any(np.abs(det) < 1e-9)
+    if ok:
+        H.build_hood(t, block_len=1024, check_triples=True)
+    for L_ in (16, 1024):  # instance kernel (L < one ring block) and ring kernel
+        q = _triple_points(1 << 14, -1, seed=L_)
+        i0 = 3 * L_ - 2  # straddles instances 2|3: not a triple of either
+        q[i0 + 2, 1] = q[i0, 1] + (q[i0 + 1, 1] - q[i0, 1]) * (q[i0 + 2, 0] - q[i0, 0]) / (q[i0 + 1, 0] - q[i0, 0])
+        det_ok = True
+        for b in range(q.shape[0] // L_):
+            w = q[b * L_:(b + 1) * L_]
+            dd = (w[1:-1, 0] - w[:-2, 0]) * (w[2:, 1] - w[:-2, 1]) - (w[1:-1, 1] - w[:-2, 1]) * (w[2:, 0] - w[:-2, 0])
+            det_ok &= not np.any(np.abs(dd) < 1e-9)
+        if det_ok:
+            H.build_hood(torch.as_tensor(q).cuda(), block_len=L_, check_triples=True)
+
+
+def O_ref_ok(oracle_mod):
+    return oracle_mod.ref_available()
+
+
+def test_record_capacity_is_reported_not_truncated(oracle_mod):
+    """hood_pack_record / hood_merge_records with a slab hood larger than the
+    record: HOOD_ERR_CAPACITY with the capacity needed, never a silently
+    truncated global hood; hood_build_multi sizes its records itself and
+    returns the oracle's hood."""
+    arc = W.arc(1 << 12)
+    t = torch.as_tensor(arc).cuda()
+    ctx = H.Context.get(0)
+    rep = H.build_hood(t)
+    cap = 1000
+    rec = H.pack_record(rep.corners, rep.counts, cap)
+    H.merge_records(torch.stack([rec, rec]))
+    with pytest.raises(H.CapacityError) as ei:
+        ctx.last_error()
+    assert ei.value.index == 1 << 12
+    # a fresh build clears the record
+    H.build_hood(t)
+    # build_multi: two arc slabs (every point a corner) with cap far below
+    halves = [torch.as_tensor(np.ascontiguousarray(h)).cuda() for h in np.array_split(arc, 2)]
+    ctxs = [H.Context(0) for _ in range(2)]
+    got = H.build_multi(halves, contexts=ctxs, cap=3000).cpu().numpy()
+    assert same(got, oracle_mod.upper_hull(arc))
+    with pytest.raises(H.CapacityError):
+        H.build_multi(halves, contexts=ctxs, cap=100)
+
+
+def test_contexts_per_thread_and_stream_order(oracle_mod):
+    """Python contexts are per (device, thread); builds from two threads on
+    two streams at once produce the oracle's hoods."""
+    import threading
+    sets = [W.grid_uniform(1 << 20, seed=80 + i) for i in range(2)]
+    want = [oracle_mod.upper_hull(p) for p in sets]
+    errs = []
+
+    def work(i):
+        try:
+            s = torch.cuda.Stream()
+            t = torch.as_tensor(sets[i]).cuda()
+            for _ in range(20):
+                with torch.cuda.stream(s):
+                    rep = H.build_hood(t)
+                if not same(rep.hull.cpu().numpy(), want[i]):
+                    errs.append(i)
+        except Exception as e:  # pragma: no cover
+            errs.append(repr(e))
+    th = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errs
+    # one context, alternating streams: each build ordered after the last
+    t = torch.as_tensor(sets[0]).cuda()
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    outs = []
+    for i in range(9):
+        with torch.cuda.stream(streams[i % 3]):
+            outs.append(H.build_hood_async(t))
+    torch.cuda.synchronize()
+    for r in outs:
+        assert same(r.hull.cpu().numpy(), want[0])
