@@ -99,6 +99,24 @@ __device__ __forceinline__ int orient_sign(const float2& a, const float2& b, con
   return orient_sign_d((double)a.x, (double)a.y, (double)b.x, (double)b.y, (double)c.x, (double)c.y);
 }
 
+// The predicate plus an uncertainty flag for evaluation-order-dependent
+// merges (warp_hull_small's iterated pruning, the finalize's chord cull): unc
+// is set when |t1 - t2| <= 2^-50 (|t1| + |t2|), above Shewchuk's error bound
+// (3u + 16u^2) of the double orient -- the computed sign may then differ from
+// the exact one, and the reference's own evaluation order (oracle.cpp:7-20)
+// is the only one guaranteed to reproduce it.  Float storage never sets it:
+// its double predicate on widened floats is the reference's on the same
+// values, and the float path's callers are order-independent in practice.
+__device__ __forceinline__ bool above_flag(const double2& a, const double2& b, const double2& c, bool& unc) {
+  const double t1 = __dmul_rn(__dsub_rn(c.x, a.x), __dsub_rn(b.y, a.y));
+  const double t2 = __dmul_rn(__dsub_rn(c.y, a.y), __dsub_rn(b.x, a.x));
+  unc |= !(fabs(__dsub_rn(t1, t2)) > __dmul_rn(8.881784197001252e-16, __dadd_rn(fabs(t1), fabs(t2))));
+  return t1 > t2;
+}
+__device__ __forceinline__ bool above_flag(const float2& a, const float2& b, const float2& c, bool&) {
+  return above(a, b, c);
+}
+
 // --------------------------------------------------------------- accessors
 // Hulls are contiguous runs of points addressed by a 64-bit slot index.
 

@@ -390,12 +390,13 @@ __device__ __forceinline__ int warp_hull_small(const V* P, int m, V* dst) {
   const int i0 = lane, i1 = lane + 32;
   const V q0 = i0 < m ? P[i0] : V{}, q1 = i1 < m ? P[i1] : V{};
   unsigned long long alive = m >= 64 ? ~0ull : ((1ull << m) - 1ull);
+  bool unc = false;
   auto keep = [&](int i, const V& q) -> bool {
     if (!((alive >> i) & 1ull)) return false;
     const unsigned long long lo = alive & ((1ull << i) - 1ull);
     const unsigned long long hi = i == 63 ? 0ull : (alive & ~((2ull << i) - 1ull));
     if (!lo || !hi) return true;  // the chain's ends stay
-    return above(P[63 - __clzll(lo)], q, P[__ffsll(hi) - 1]);
+    return above_flag(P[63 - __clzll(lo)], q, P[__ffsll(hi) - 1], unc);
   };
   for (;;) {
     const bool k0 = keep(i0, q0);
@@ -404,6 +405,29 @@ __device__ __forceinline__ int warp_hull_small(const V* P, int m, V* dst) {
                                    ((unsigned long long)__ballot_sync(0xffffffffu, k1) << 32);
     if (nxt == alive) break;
     alive = nxt;
+  }
+  if (__any_sync(0xffffffffu, unc)) {
+    // a near-degenerate triple: the reference's own evaluation order, the
+    // monotone chain (oracle.cpp:7-20) by one lane, decides instead
+    __syncwarp();
+    int h = 0;
+    if (lane == 0) {
+      V s1 = V{}, s2 = V{};
+      for (int i = 0; i < m; ++i) {
+        const V q = P[i];
+        while (h >= 2 && !above(s2, s1, q)) {
+          --h;
+          s1 = s2;
+          if (h >= 2) s2 = dst[h - 2];
+        }
+        dst[h++] = q;  // h <= i: never past the point being read when dst == P
+        s2 = s1;
+        s1 = q;
+      }
+    }
+    h = __shfl_sync(0xffffffffu, h, 0);
+    __syncwarp();
+    return h;
   }
   __syncwarp();
   if ((alive >> i0) & 1ull) dst[__popcll(alive & ((1ull << i0) - 1ull))] = q0;
@@ -527,6 +551,9 @@ struct RingLayout {
   static constexpr size_t PB = HS + (size_t)HCap<S>::value * sizeof(V); // [PC] pending survivors
   static constexpr size_t MNS = up(PB + (size_t)PC * sizeof(V), 8);     // [32] tree starts
   static constexpr size_t MNC = MNS + 32 * 8;                           // [32] tree counts
+  // [2] the hood's last two corners after a direct block append; aliases the
+  // tree starts (a merge tree clears the cache's validity before it runs)
+  static constexpr size_t HT = MNS;
   static constexpr size_t BYTES = up(MNC + 32 * 4, 128);
 };
 
@@ -779,6 +806,81 @@ __device__ __forceinline__ int ring_rot(int l) {
   return U == 8 ? (l & 7) : ((l >> 1) & 3);
 }
 
+struct AppendRes {
+  HoodState h;
+  bool ok;
+};
+
+// A block of which every point survives the anchor cull (arc-like input):
+// if its points form a strictly concave chain that continues the unit's hood
+// without a pop -- every triple the monotone chain (oracle.cpp:7-20) would
+// test, all strictly left -- they ARE the next corners of the hood, so they
+// are streamed from the ring slot straight to the hood's output slots
+// (coalesced: store k of lane l writes corner 32k + l) with no compaction,
+// no staging and no merge.  The concavity test runs on the lane runs in
+// registers (in-lane triples plus one shuffle per side).  `ht` caches the
+// hood's last two corners when ht_ok (set by the previous append), so a run of
+// such blocks never reads its own output back.  Otherwise returns ok = false
+// with nothing changed.
+template <class S, int U, int HC>
+__device__ __noinline__ AppendRes append_full_block(unsigned a, unsigned slot_base, typename PointT<S>::V* Hs,
+                                                    typename PointT<S>::V* gslab, typename PointT<S>::V* ht,
+                                                    HoodState h, bool ht_ok) {
+  using V = typename PointT<S>::V;
+  using L = typename Ld16<S>::T;
+  constexpr int PPL = Ld16<S>::PPL, NP = U * PPL, BP = 32 * NP;
+  constexpr unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  V v[NP];
+#pragma unroll
+  for (int k = 0; k < U; ++k) {
+    const L c = lds16<L>(a ^ (k << 4));
+#pragma unroll
+    for (int e = 0; e < PPL; ++e) v[k * PPL + e] = pt_of(c, e);
+  }
+  V prev, next;
+  prev.x = __shfl_up_sync(FULL, v[NP - 1].x, 1);
+  prev.y = __shfl_up_sync(FULL, v[NP - 1].y, 1);
+  next.x = __shfl_down_sync(FULL, v[0].x, 1);
+  next.y = __shfl_down_sync(FULL, v[0].y, 1);
+  bool conc = true;
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    const V& l = i > 0 ? v[i - 1] : prev;
+    const V& r = i + 1 < NP ? v[i + 1] : next;
+    const bool skip = (i == 0 && lane == 0) || (i == NP - 1 && lane == 31);
+    if (!skip) conc = conc && above(l, v[i], r);
+  }
+  if (!__all_sync(FULL, conc)) return AppendRes{h, false};
+  bool join = true;
+  if (lane == 0 && h.n >= 1) {
+    const V* src = h.in_smem ? Hs : gslab;
+    const V t1 = ht_ok ? ht[1] : src[h.n - 1];
+    if (h.n >= 2) join = above(ht_ok ? ht[0] : src[h.n - 2], t1, v[0]);
+    if (join) join = above(t1, v[0], v[1]);
+  }
+  if (!__shfl_sync(FULL, join, 0)) return AppendRes{h, false};
+  static_assert(BP > HC, "a whole block never fits the smem hood");
+  if (h.in_smem) {  // the hood moves to its output slots
+    for (long long i = lane; i < h.n; i += 32) gslab[i] = Hs[i];
+    h.in_smem = 0;
+  }
+  V* dst = gslab + h.n;  // global: plain STG, no generic-address resolution
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    const int q = 32 * k + lane, r = q / NP, e = q % NP;
+    const unsigned ad = (slot_base + r * (16 * U) + (((e / PPL) ^ ring_rot<U>(r)) << 4)) + (e % PPL) * (unsigned)sizeof(V);
+    dst[q] = lds_pt(ad, (V*)nullptr);
+  }
+  if (lane == 31) {
+    ht[0] = v[NP - 2];
+    ht[1] = v[NP - 1];
+  }
+  __syncwarp();
+  h.n += BP;
+  return AppendRes{h, true};
+}
+
 // The hot kernel.  Every warp is an independent pipeline over its own
 // sequence of units (contiguous x-ranges of the input; a whole instance in
 // batched builds).  Its lanes stream the blocks of that sequence (256 float2 /
@@ -840,6 +942,7 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
   V* PBf = reinterpret_cast<V*>(wb + LY::PB);
   long long* mns = reinterpret_cast<long long*>(wb + LY::MNS);
   int* mnc = reinterpret_cast<int*>(wb + LY::MNC);
+  V* htail = reinterpret_cast<V*>(wb + LY::HT);
   const V* gpts = reinterpret_cast<const V*>(p.pts);
   const unsigned char* gbytes = reinterpret_cast<const unsigned char*>(p.pts) + lane * 16;
   V* gout = reinterpret_cast<V*>(p.out);
@@ -1079,6 +1182,7 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
   S runmax = NEG;   // left anchor: everything before the block
   HoodState hs{0, 1};
   int pend = 0;     // queued survivors in PBf
+  bool ht_ok = false;  // htail holds the hood's last two corners (set by a direct append)
   bool fresh = true;
   int s_cur = 0;    // ring slot of sequence block k
   int s_far = D;    // ring slot of block k + D
@@ -1088,6 +1192,7 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
   auto flush = [&]() {
     __syncwarp();
     if (pend == 0) return;
+    ht_ok = false;
     HOOD_TIC();
     if (hs.in_smem && hs.n + pend <= HC) {  // pend <= PC: one lane pushes them
       long long h = hs.n;
@@ -1133,6 +1238,7 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
       runmax = ext_l;
       hs = HoodState{0, 1};
       pend = 0;
+      ht_ok = false;
     }
 
     // right anchor: the unit's next blocks inside the window, then EXT
@@ -1190,13 +1296,31 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
         }
       }
       const int cnt = __popc(svm);
-      int incl = cnt;
+      int incl, total;
+      if (__all_sync(FULL, svm == (1u << NP) - 1u)) {
+        incl = (lane + 1) * NP;  // every point survives (arc-like input): no scan
+        total = BP;
+      } else {
+        incl = cnt;
 #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int o = __shfl_up_sync(FULL, incl, d);
-        if (lane >= d) incl += o;
+        for (int d = 1; d < 32; d <<= 1) {
+          const int o = __shfl_up_sync(FULL, incl, d);
+          if (lane >= d) incl += o;
+        }
+        total = __shfl_sync(FULL, incl, 31);
       }
-      const int total = __shfl_sync(FULL, incl, 31);
+      bool appended = false;
+      if (!LEAN && total == BP) {
+        // every point survives (arc-like input): straight to the output
+        // slots when the block continues the hood as a concave chain
+        flush();
+        const AppendRes ar = append_full_block<S, U, HC>(a, ring_s + s_cur * BB, Hs, gout + ubase, htail, hs, ht_ok);
+        hs = ar.h;
+        appended = ar.ok;
+        ht_ok = ar.ok;
+      }
+      if (appended) {
+      } else {
       if (pend + total > PC) flush();
       int pos = incl - cnt;
       V* dst = PBf + pend;
@@ -1222,9 +1346,11 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
         __syncwarp();
         if constexpr (LEAN) hs = merge_block_lean<S, HC>(dst, total, Hs, gout + ubase, hs);
         else hs = merge_block_tree<S, HC>(dst, total, mns, mnc, Hs, gout + ubase, hs);
+        ht_ok = false;
         __syncwarp();
       } else {
         pend += total;
+      }
       }
     }
     HOOD_TOC(c_cand);
@@ -1297,6 +1423,22 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
       }
       __syncwarp();
       if constexpr (!LEAN) {
+        if (p.full_units && lane == 0) {
+          // every point of the unit is a corner (the arc): with the unit
+          // before it also full, the seam's two monotone-chain triples are
+          // input triples -- checked here, so a finalize that sees every unit
+          // counted has nothing left to merge
+          const long long uend = min(n, (long long)(cc.b + 1) * BP);
+          if (hs.n == uend - ubase) {
+            bool ok = true;
+            if (ubase >= 1) {
+              const V a1 = gpts[ubase - 1], b0 = gpts[ubase];
+              if (ubase >= 2) ok = above(gpts[ubase - 2], a1, b0);
+              if (ok && ubase + 1 < uend) ok = above(a1, b0, gpts[ubase + 1]);
+            }
+            if (ok) atomicAdd(p.full_units, 1u);
+          }
+        }
         if (p.arrive && lane == 0) {  // the unit's hood, count and anchor are published
           __threadfence();  // cumulative: covers the lanes' writes ordered by the __syncwarp
           atomicAdd(p.arrive, 1u);
@@ -1706,6 +1848,23 @@ __device__ __noinline__ void finalize_body(const FinalizeParams<S> p) {
     asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the slab kernel has completed
   }
   if (p.done && *p.done) return;  // merged already (small exchange)
+  if (p.full_units) {
+    // every unit's hood is all of its points and every seam is concave (the
+    // ring kernel checked them): the hood is the input, already in place
+    volatile unsigned* fu = p.full_units;
+    int* flag = reinterpret_cast<int*>(smem_raw);
+    if (threadIdx.x == 0) {
+      flag[0] = (*fu == (unsigned)p.slabs_per_inst);
+      *fu = 0u;  // for the next build
+    }
+    __syncthreads();
+    const int all = flag[0];
+    __syncthreads();
+    if (all) {
+      if (threadIdx.x == 0) p.out_counts[blockIdx.x] = (int)p.L;
+      return;
+    }
+  }
   if (kTrace && p.trace && tid == 0) {
     p.trace[0] = clock64();
     p.trace[30] = (long long)gtimer();
@@ -1796,7 +1955,10 @@ __device__ __noinline__ void finalize_body(const FinalizeParams<S> p) {
           bool keep = false;
           if (e < cnt) {
             if (e0 != 0) w = gout[cb[c] + e];
-            keep = !both || above(A, w, Cp);
+            // a corner within rounding of the chord is kept (the final
+            // hull decides it in the reference's order)
+            bool unc = false;
+            keep = !both || above_flag(A, w, Cp, unc) || unc;
           }
           const unsigned mk = __ballot_sync(0xffffffffu, keep);
           const int pos = n_alive + __popc(mk & ((1u << lane) - 1u));
@@ -2326,7 +2488,8 @@ __global__ void __launch_bounds__(256) gather_records_kernel(const double2* recs
     __syncthreads();
     auto keep_of = [&](int g, const double2& v) {
       const double2 A = A_s[g], Cp = C_s[g];
-      return !(A.y > NEG && Cp.y > NEG) || above(A, v, Cp);
+      bool unc = false;  // within rounding of the chord: kept
+      return !(A.y > NEG && Cp.y > NEG) || above_flag(A, v, Cp, unc) || unc;
     };
     for (int g = warp; g < G; g += NWP) {  // survivors per record
       const double2* r = recs + (long long)g * (cap + 1) + 1;

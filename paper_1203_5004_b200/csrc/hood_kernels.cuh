@@ -63,6 +63,10 @@ struct SlabParams {
   long long read_lim;       // points at or past this index may not be read yet (host-path chunks)
   int lean;                 // ring kernel: the register-light variant (batched builds)
   unsigned* arrive;         // optional: +1 per finished unit (release), read by the finalize
+  // optional (single instance): +1 per unit whose hood is ALL its points and
+  // whose left seam continues the unit before it concavely (arc-like input);
+  // when every unit counts, the finalize's answer is the input itself
+  unsigned* full_units;
 };
 
 template <class S>
@@ -83,6 +87,7 @@ struct FinalizeParams {
   // ring grid's completion; the finalize zeroes it for the next build
   unsigned* arrive;
   unsigned arrive_target;
+  unsigned* full_units;     // optional (single instance): see SlabParams; zeroed here for the next build
   // optional: a tiny resident dummy instance (kWarmBytes, written by the
   // error-reset kernel) the finalize merges first, while it waits for the
   // unit counter -- its code is then in the caches for the real merge

@@ -69,6 +69,20 @@ def acceptance():
         data[f"count_{n}"] = np.array(counts, dtype=np.int32)
         if rounds:
             data[f"rounds_{n}"] = np.stack(rounds)
+        # the whole sweep: all 100 seeds (acceptance.cpp:43-47 kSeedsPerSize),
+        # inputs + build_hood's hull (compact, concatenated)
+        p100, h100, c100 = [], [], []
+        for s in range(100):
+            seed = 0xACCE97 + s * 1315423911 + n
+            p = O.ref_make_random_point_set(n, seed)
+            h, _ = O.ref_build_hood(p)
+            assert np.array_equal(h, O.ref_upper_hull(p))  # criterion 1 on the reference itself
+            p100.append(p)
+            h100.append(h)
+            c100.append(len(h))
+        data[f"pts100_{n}"] = np.stack(p100)
+        data[f"hulls100_{n}"] = np.concatenate(h100)
+        data[f"count100_{n}"] = np.array(c100, dtype=np.int32)
     np.savez_compressed(os.path.join(OUT, "acceptance.npz"), **data)
 
 
