@@ -323,11 +323,11 @@ def run_ours(args):
 
     desc, n_global, storage, block, make = workload(args.config, args.log2n)
     # this rank's contiguous slab of the one global set (x already global)
+    from paper_1203_5004_b200.distributed import slab_range
     full = make(dev)
-    n = n_global // world
-    if block and n % block:
-        raise SystemExit(f"{n_global // block} instances do not split over {world} ranks")
-    pts = full[rank * n:(rank + 1) * n].clone() if world > 1 else full
+    lo, hi = slab_range(n_global, world, rank, block)
+    n = hi - lo
+    pts = full[lo:hi].clone() if world > 1 else full
     del full
     torch.cuda.empty_cache()
     f64 = pts.dtype == torch.float64

@@ -166,6 +166,12 @@ int hood_merge_round_scratch_f32(hood_ctx* ctx, const float* d_in, int64_t n, in
 int hood_merge_round_scratch_f64(hood_ctx* ctx, const double* d_in, int64_t n, int64_t d, double* d_out,
                                  int32_t* d_scratch, void* stream);
 
+/* The same round from host buffers (n double2 slots in, n out), synchronous:
+ * the drop-in build_hood's observer mode runs the reference round loop this
+ * way.  Returns HOOD_ERR_DEGENERATE (index via
+ * hood_last_error = the block) where the reference throws DegenerateTangent. */
+int hood_merge_round_host_f64(hood_ctx* ctx, const double* h_in, int64_t n, int64_t d, double* h_out);
+
 /* Synchronizes the stream of the last build and reports its first error:
  * validation (x range / order, then the consecutive-triple margin) before a
  * record capacity shortfall (HOOD_ERR_CAPACITY, index = capacity needed). */

@@ -873,6 +873,28 @@ int hood_merge_round_scratch_f64(hood_ctx* ctx, const double* d_in, int64_t n, i
   return merge_round<double>(ctx, d_in, n, d, d_out, d_scratch, reinterpret_cast<cudaStream_t>(stream));
 }
 
+// One reference round from host buffers (the observer mode of the drop-in
+// build_hood): H2D, hood_merge_round, D2H,
+// synchronous; a degenerate tangent comes back as HOOD_ERR_DEGENERATE with
+// hood_last_error().index = the block.
+int merge_round_host(hood_ctx* ctx, const double* h_in, long long n, long long d, double* h_out) {
+  if (!ctx || !h_in || !h_out) return HOOD_ERR_INVALID_ARG;
+  if (d < 1 || (d & (d - 1)) != 0 || n < 2 * d || n % (2 * d) != 0) return HOOD_ERR_INVALID_ARG;
+  cudaSetDevice(ctx->device);
+  int rc;
+  if ((rc = ensure_host_bufs<double>(ctx, n, 1))) return rc;
+  const size_t bytes = (size_t)n * 2 * sizeof(double);
+  cudaStream_t sk = ctx->s_comp;
+  order_after_last(ctx, sk);
+  if (cudaMemcpyAsync(ctx->d_in, h_in, bytes, cudaMemcpyHostToDevice, sk) != cudaSuccess) return HOOD_ERR_CUDA;
+  if ((rc = merge_round<double>(ctx, reinterpret_cast<const double*>(ctx->d_in), n, d,
+                                reinterpret_cast<double*>(ctx->d_out), nullptr, sk)))
+    return rc;
+  if (cudaMemcpyAsync(h_out, ctx->d_out, bytes, cudaMemcpyDeviceToHost, sk) != cudaSuccess) return HOOD_ERR_CUDA;
+  hood_error e;
+  return decode_error(ctx, &e);
+}
+
 // The round trace of build_hood (cli.cpp:163-166 observer + write_trace_round,
 // cli.cpp:108-118): the input is the HoodBuffer at d = 2 (init_hood,
 // hoodbuf.cpp:88-92); each round is formatted, then merged on the GPU.
@@ -905,6 +927,10 @@ int hood_write_trace_f64(hood_ctx* ctx, const double* h_pts, int64_t n, const ch
   cudaFree(d_a);
   cudaFree(d_b);
   return rc;
+}
+
+int hood_merge_round_host_f64(hood_ctx* ctx, const double* h_in, int64_t n, int64_t d, double* h_out) {
+  return merge_round_host(ctx, h_in, n, d, h_out);
 }
 
 int hood_create(hood_ctx** out, int device) {

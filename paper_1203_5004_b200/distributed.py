@@ -32,6 +32,24 @@ from typing import Callable, Optional
 DEFAULT_CAP = 4096
 
 
+def slab_range(n_global: int, world: int, rank: int, block_len: int = 0):
+    """[lo, hi) of rank's contiguous x-slab of ONE global x-sorted set of
+    n_global points (contiguous slabs of n/G, G a power of
+    two, so slabs are reference round-blocks); batched sets (block_len > 0)
+    split on instance boundaries.  The slab keeps its global coordinates, so
+    the exchange needs no x offset (exact for double2 as well as float2)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world / rank")
+    unit = block_len if block_len else 1
+    if n_global % unit:
+        raise ValueError("n_global must be a multiple of block_len")
+    units = n_global // unit
+    if units % world:
+        raise ValueError(f"{units} {'instances' if block_len else 'points'} do not split over {world} ranks")
+    per = units // world
+    return rank * per * unit, (rank + 1) * per * unit
+
+
 @dataclass
 class ShardResult:
     hull: "object"          # (k, 2) float64 tensor: the global hood, left to right
@@ -105,8 +123,10 @@ def sharded_build(points, group=None, cap: int = DEFAULT_CAP, x_offset: float = 
 
     points   this rank's slab, (n_r, 2), x strictly increasing, every x left of
              the next rank's slab (after adding x_offset).
-    x_offset added to this rank's x (exactly, in float64) to form global x; the
-             weak-scaling bench gives every rank a slab in (0, 1) and offset = rank.
+    x_offset added to this rank's x in float64 to form global x: exact for
+             float2 slabs (a float widened to double plus a small integer);
+             double2 slabs should be cut from one global set (slab_range) and
+             use offset 0, as bench.py does.
     """
     import torch
 

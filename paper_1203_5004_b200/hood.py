@@ -45,7 +45,7 @@ EXPORTS = [
     "hood_format_section", "hood_format_trace_round", "hood_write_trace_f64",
     "hood_pack_record_f32", "hood_pack_record_f64", "hood_merge_records",
     "hood_build_multi_f32", "hood_build_multi_f64",
-    "hood_merge_round_scratch_f32", "hood_merge_round_scratch_f64",
+    "hood_merge_round_scratch_f32", "hood_merge_round_scratch_f64", "hood_merge_round_host_f64",
 ]
 
 
@@ -97,6 +97,7 @@ def library():
             for nm in ("hood_pack_record_f32", "hood_pack_record_f64"):
                 getattr(L, nm).argtypes = [p, p, p, i64, ctypes.c_double, p, p]
             L.hood_merge_records.argtypes = [p, p, i64, i64, p, p, p]
+            L.hood_merge_round_host_f64.argtypes = [p, p, i64, i64, p]
             for nm in ("hood_build_multi_f32", "hood_build_multi_f64"):
                 getattr(L, nm).argtypes = [p, ctypes.c_int, p, p, p, p, p, i64]
             L.hood_last_error.argtypes = [p, ctypes.POINTER(_Err)]

@@ -27,7 +27,15 @@ def _slab(rank: int, n: int, arc: bool):
     return W.arc(n) if arc else W.grid_uniform(n, seed=100 + rank)
 
 
-def _worker(rank, world, port, n, cap, arc, q):
+def _global_slab(rank: int, world: int, n_global: int):
+    """bench.py's split: rank's contiguous slab of ONE config-4-shaped set."""
+    from paper_1203_5004_b200 import workloads as W
+    from paper_1203_5004_b200.distributed import slab_range
+    lo, hi = slab_range(n_global, world, rank)
+    return W.gauss(n_global, seed=4)[lo:hi]
+
+
+def _worker(rank, world, port, n, cap, arc, q, global_set=False):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import torch
@@ -40,7 +48,7 @@ def _worker(rank, world, port, n, cap, arc, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        pts = _slab(rank, n, arc)
+        pts = _global_slab(rank, world, n) if global_set else _slab(rank, n, arc)
 
         def build_local(p):
             h = O.upper_hull(np.asarray(p, dtype=np.float64))
@@ -50,19 +58,19 @@ def _worker(rank, world, port, n, cap, arc, q):
             cat = np.concatenate([segs[g, : int(counts[g])].numpy() for g in range(segs.shape[0])])
             return torch.from_numpy(O.upper_hull(cat))
 
-        res = Dz.sharded_build(torch.from_numpy(pts), cap=cap, x_offset=float(rank),
+        res = Dz.sharded_build(torch.from_numpy(pts), cap=cap, x_offset=0.0 if global_set else float(rank),
                                build_local=build_local, merge=merge)
         q.put((rank, res.hull.numpy(), res.slab_counts, res.exchanges))
     finally:
         dist.destroy_process_group()
 
 
-def _run(world, n, cap, arc):
+def _run(world, n, cap, arc, global_set=False):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, n, cap, arc, q)) for r in range(world)]
+    ps = [ctx.Process(target=_worker, args=(r, world, port, n, cap, arc, q, global_set)) for r in range(world)]
     for p in ps:
         p.start()
     out = [q.get(timeout=120) for _ in range(world)]
@@ -104,3 +112,32 @@ def test_pack_record_layout():
     assert rec.shape == (5, 2) and rec.dtype == torch.float64
     assert rec[0, 0] == 2
     assert rec[1, 0] == 3.25 and rec[2, 1] == 0.75 and rec[3, 0] == 0
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_bench_split_of_one_global_set(oracle_mod, world):
+    """bench.py under torchrun: ONE global config-4-shaped set (Gaussian
+    double2, x global) cut by slab_range into contiguous slabs, no x offset;
+    every rank ends with the global set's hood."""
+    from paper_1203_5004_b200 import workloads as W
+    n = 1 << 14
+    out = _run(world, n, cap=512, arc=False, global_set=True)
+    want = oracle_mod.upper_hull(W.gauss(n, seed=4))
+    for rank, hull, counts, ex in out:
+        assert ex == 1 and len(counts) == world
+        np.testing.assert_array_equal(hull, want)
+
+
+def test_slab_range_partitions():
+    from paper_1203_5004_b200.distributed import slab_range
+    for n, world, block in [(1 << 28, 8, 0), (1 << 30, 8, 0), (1 << 28, 2, 0), (65536 * 1024, 4, 1024)]:
+        rs = [slab_range(n, world, r, block) for r in range(world)]
+        assert rs[0][0] == 0 and rs[-1][1] == n
+        assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+        assert len({hi - lo for lo, hi in rs}) == 1
+        if block:
+            assert all(lo % block == 0 for lo, _ in rs)
+    with pytest.raises(ValueError):
+        slab_range(1000, 3, 0)
+    with pytest.raises(ValueError):
+        slab_range(1024 * 3, 2, 0, 1024)

@@ -4,6 +4,8 @@ Bit-exact comparison of corner coordinates (corners are selections of input
 points; hood_b200.h).  Golden vectors restate the reference's own tests with
 file:line; the fixtures come from the reference itself (tests/golden/).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -961,3 +963,50 @@ def test_acceptance_full_sweep_100_seeds(golden, dtype):
             assert same(corners[s * n: s * n + c[s]], want), (n, s)
             if s % 10 == 0:
                 assert same(gpu_hull(pts[s]), want), (n, s)
+
+
+# ----------------------------- the reference's own harness through the drop-in
+
+DROPIN = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_dropin")
+
+
+def _run_bin(name, timeout=600):
+    import subprocess
+    path = os.path.join(DROPIN, name)
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not built (oracle/dropin/build_dropin.py needs the reference tree)")
+    r = subprocess.run([path], capture_output=True, text=True, timeout=timeout)
+    return r.returncode, r.stdout + r.stderr
+
+
+def test_reference_acceptance_through_dropin():
+    """proj/tests/acceptance.cpp, unmodified, linked against driver.cpp with
+    the HOOD_USE_B200 binding (oracle/dropin):
+    criteria 1-3 run the 900-run sweep with an on_round_end observer, i.e.
+    the reference round loop with every round merged on the GPU
+    (hood_merge_round_host_f64); criterion 8 builds through hood_build_host.
+    Every criterion must come out exactly as it does for the unpatched
+    reference (acceptance_ref) -- criterion 4 is a psim-kernel property the
+    reference itself fails (sample corners stepping left, test_kernel.cpp
+    "tangent corners can step left"), untouched by the drop-in."""
+    rc_ref, out_ref = _run_bin("acceptance_ref")
+    rc, out = _run_bin("acceptance")
+
+    def verdicts(text):
+        return {ln.split(":")[0].split()[-1]: ln.split()[0] for ln in text.splitlines()
+                if ln.startswith(("PASS criterion", "FAIL criterion"))}
+    got, want = verdicts(out), verdicts(out_ref)
+    assert set(got) == {str(i) for i in range(1, 9)}, out
+    assert got == want, (out, out_ref)
+    for c in ("1", "2", "3", "5", "6", "7", "8"):
+        assert got[c] == "PASS", out
+    assert "900 runs" in out and "0 mismatches" in out
+
+
+@pytest.mark.parametrize("name", ["test_driver", "test_cli"])
+def test_reference_unit_tests_through_dropin(name):
+    """proj/tests/test_driver.cpp (build_hood with and without observers,
+    round_metrics formulas) and test_cli.cpp (cli::run -> build_hood, trace
+    observer) against the drop-in, with a minimal doctest stand-in."""
+    rc, out = _run_bin(name)
+    assert rc == 0 and "0 failed" in out, out
