@@ -594,10 +594,14 @@ __device__ __forceinline__ unsigned long long l2_evict_first_policy() {
 }
 template <class L>
 __device__ __forceinline__ L lds16(unsigned a);
+// ld.volatile: a caller that uses only the y values would otherwise let
+// ptxas narrow the 16-byte load to 4/8-byte y loads, whose 128-byte lane
+// stride is a 4-way bank conflict (ncu config 5: 6.4M conflicts, all in
+// edge_survivors); a volatile load keeps its width.
 template <>
 __device__ __forceinline__ float4 lds16<float4>(unsigned a) {
   float4 v;
-  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+  asm volatile("ld.volatile.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                : "r"(a)
                : "memory");
@@ -606,7 +610,7 @@ __device__ __forceinline__ float4 lds16<float4>(unsigned a) {
 template <>
 __device__ __forceinline__ double2 lds16<double2>(unsigned a) {
   double2 v;
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+  asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
   return v;
 }
 __device__ __forceinline__ float2 lds_pt(unsigned a, float2*) {
@@ -1761,17 +1765,26 @@ constexpr int kFinCandCap = 32;    // corners staged per candidate
 // code after an L2 flush, and four inlined copies cost instruction fetches).
 template <class V>
 __device__ __noinline__ void chord_run(const V* h, int c, V A, V Cp, int& l, int& r) {
+  // the peak: the first edge not steeper than the chord, comparing slopes in
+  // double (floats widen exactly; no chord direction rounded to storage)
+  const double cx = (double)Cp.x - (double)A.x, cy = (double)Cp.y - (double)A.y;
   int a = 0, bq = c - 1;
   while (a < bq) {
     const int mid = (a + bq) >> 1;
-    const V d = V{h[mid].x + (Cp.x - A.x), h[mid].y + (Cp.y - A.y)};
-    if (orient_sign(h[mid], h[mid + 1], d) > 0) a = mid + 1;
+    const double ex = (double)h[mid + 1].x - (double)h[mid].x, ey = (double)h[mid + 1].y - (double)h[mid].y;
+    if (__dmul_rn(ey, cx) > __dmul_rn(cy, ex)) a = mid + 1;
     else bq = mid;
   }
-  const int pk = a;
+  int pk = a;
   if (!above(A, h[pk], Cp)) {
-    l = r = 0;
-    return;
+    // a slope comparison within rounding can land one corner off the peak:
+    // its neighbours decide before the run is declared empty
+    if (pk > 0 && above(A, h[pk - 1], Cp)) pk = pk - 1;
+    else if (pk + 1 < c && above(A, h[pk + 1], Cp)) pk = pk + 1;
+    else {
+      l = r = 0;
+      return;
+    }
   }
   int x0 = 0, x1 = pk;
   while (x0 < x1) {
