@@ -546,15 +546,21 @@ struct RingLayout {
   static constexpr int BP = 32 * U * Ld16<S>::PPL;                      // points per block
   static constexpr size_t BB = 32 * U * 16;                             // bytes per block
   static constexpr int PC = 64;                                         // pending survivor capacity
-  static constexpr size_t RING = 0;                                     // [R] blocks
-  static constexpr size_t HS = RING + (size_t)R * BB;                   // [HC] running unit hood
+  // The CTA's rings come first, warp w's at w * RINGB: every slot starts on a
+  // 1024-byte boundary (the 128B-swizzle atom of a TMA tile, whose row r of
+  // 128 bytes holds its 16-byte unit u at u ^ (r & 7) -- exactly the lane-run
+  // swizzle of ring_rot).  Then each warp's own state:
+  static constexpr size_t RINGB = (size_t)R * BB;
+  static constexpr size_t HS = 0;                                       // [HC] running unit hood
   static constexpr size_t PB = HS + (size_t)HCap<S>::value * sizeof(V); // [PC] pending survivors
   static constexpr size_t MNS = up(PB + (size_t)PC * sizeof(V), 8);     // [32] tree starts
   static constexpr size_t MNC = MNS + 32 * 8;                           // [32] tree counts
   // [2] the hood's last two corners after a direct block append; aliases the
   // tree starts (a merge tree clears the cache's validity before it runs)
   static constexpr size_t HT = MNS;
-  static constexpr size_t BYTES = up(MNC + 32 * 4, 128);
+  static constexpr size_t BAR = up(MNC + 32 * 4, 8);                    // [R] slot mbarriers (TMA ring)
+  static constexpr size_t BYTES = up(BAR + (size_t)R * 8, 16);          // per-warp state
+  static constexpr size_t CTA_BYTES(int warps) { return (size_t)warps * (RINGB + BYTES); }
 };
 
 // Warp inclusive max-scans (toward higher lanes / toward lower lanes).
@@ -594,14 +600,14 @@ __device__ __forceinline__ unsigned long long l2_evict_first_policy() {
 }
 template <class L>
 __device__ __forceinline__ L lds16(unsigned a);
-// ld.volatile: a caller that uses only the y values would otherwise let
-// ptxas narrow the 16-byte load to 4/8-byte y loads, whose 128-byte lane
-// stride is a 4-way bank conflict (ncu config 5: 6.4M conflicts, all in
-// edge_survivors); a volatile load keeps its width.
+// A caller that uses only the y values lets ptxas narrow these 16-byte loads
+// to 4/8-byte y loads, whose 128-byte lane stride is a 4-way bank conflict
+// (ncu config 5, round 1: 6.4M conflicts, all in edge_survivors): see
+// keep_width() there.
 template <>
 __device__ __forceinline__ float4 lds16<float4>(unsigned a) {
   float4 v;
-  asm volatile("ld.volatile.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                : "r"(a)
                : "memory");
@@ -610,7 +616,7 @@ __device__ __forceinline__ float4 lds16<float4>(unsigned a) {
 template <>
 __device__ __forceinline__ double2 lds16<double2>(unsigned a) {
   double2 v;
-  asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
   return v;
 }
 __device__ __forceinline__ float2 lds_pt(unsigned a, float2*) {
@@ -634,18 +640,23 @@ __device__ __noinline__ unsigned edge_survivors(unsigned a, long long q0, long l
   L c[U];
 #pragma unroll
   for (int k = 0; k < U; ++k) c[k] = lds16<L>(a ^ (k << 4));
+  // keep the 16-byte loads whole (no narrowed, bank-conflicting y loads):
+  // y + 0 * x is y exactly for finite x (x is validated finite and ordered;
+  // a non-finite x is an x error whatever this returns), and IEEE forbids
+  // folding 0 * x, so the x components stay live
+  auto keep_width = [](const typename PointT<S>::V& q) -> S { return q.y + (S)0 * q.x; };
   S yv[NP];
   S t = NEG;
   if (q0 + NP <= n) {  // the lane's whole run exists (every block but the input's last)
 #pragma unroll
     for (int i = 0; i < NP; ++i) {
-      yv[i] = pt_of(c[i / PPL], i % PPL).y;
+      yv[i] = keep_width(pt_of(c[i / PPL], i % PPL));
       t = fmax(t, yv[i]);
     }
   } else {
 #pragma unroll
     for (int i = 0; i < NP; ++i) {
-      yv[i] = (q0 + i < n) ? pt_of(c[i / PPL], i % PPL).y : NEG;
+      yv[i] = (q0 + i < n) ? keep_width(pt_of(c[i / PPL], i % PPL)) : NEG;
       t = fmax(t, yv[i]);
     }
   }
@@ -932,9 +943,11 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
 
   extern __shared__ unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned pad = (128u - (smem_u32(smem_raw) & 127u)) & 127u;
-  unsigned char* wb = smem_raw + pad + (size_t)warp * LY::BYTES;
-  const unsigned ring_s = smem_u32(wb + LY::RING);
+  // rings at 1024-byte boundaries (the dynamic shared window starts aligned:
+  // no static shared memory in this kernel)
+  unsigned char* wring = smem_raw + (size_t)warp * LY::RINGB;
+  unsigned char* wb = smem_raw + (size_t)(blockDim.x >> 5) * LY::RINGB + (size_t)warp * LY::BYTES;
+  const unsigned ring_s = smem_u32(wring);
   // cp.async destination of the lane's chunk in copy j: wr + j*512 (U == 4),
   // (wr + j*512) ^ ((j & 1) << 6) (U == 8)
   const unsigned wr = U == 8 ? ring_s + (lane >> 3) * 128 + (((lane & 7) ^ (lane >> 3)) << 4)
@@ -1335,7 +1348,7 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
 #pragma unroll
         for (int k = 0; k < U; ++k) c[k] = lds16<L>(a ^ (k << 4));
         __syncwarp();
-        dst = reinterpret_cast<V*>(wb + LY::RING + (size_t)s_cur * BB);
+        dst = reinterpret_cast<V*>(wring + (size_t)s_cur * BB);
 #pragma unroll
         for (int i = 0; i < NP; ++i)
           if ((svm >> i) & 1u) dst[pos++] = pt_of(c[i / PPL], i % PPL);
@@ -2570,7 +2583,7 @@ constexpr int kRingD = 1, kRingP = 1, kRingU = 8;
 
 template <class S, bool LEAN>
 static size_t ring_smem() {
-  return (size_t)kRingWarps * RingLayout<S, kRingD, kRingP, kRingU>::BYTES + 128;  // + alignment pad
+  return RingLayout<S, kRingD, kRingP, kRingU>::CTA_BYTES(kRingWarps);
 }
 
 // Per-device launch state: the dynamic shared-memory opt-in
