@@ -295,18 +295,14 @@ int build_device(hood_ctx* ctx, const S* pts, long long n, long long block_len, 
   order_after_last(ctx, st);
   CUtensorMap map;
   long long full_rows = 0;
-  std::memset(&map, 0, sizeof(map));
-  // the instance kernel's tiles; the ring kernel's when it fills by TMA (32 rows of 128 B per block)
-  const bool tma_ring = pl.hmode && ring_tma() && !(flags & HOOD_FLAG_CHECK_TRIPLES);
+  std::memset(&map, 0, sizeof(map));  // the ring kernel (hmode) fills with cp.async, no tensor map
   if (!pl.hmode && (rc = encode_map<S>(pts, n, pl.rows, &map, &full_rows))) return rc;
-  if (tma_ring && (rc = encode_map<S>(pts, n, 32, &map, &full_rows))) return rc;
   // the ring path resets the error record in-stream (launch_slab_kernel),
   // except under profile events, which bracket the ring kernel alone
   const bool reset_in_stream = pl.hmode && !ctx->prof_before;
   if (!reset_in_stream && cudaMemsetAsync(ctx->err, 0xff, sizeof(DevError), st) != cudaSuccess)
     return HOOD_ERR_CUDA;
   SlabParams<S> p = slab_params<S>(ctx, pl, pts, corners, counts, full_rows, flags);
-  p.ring_tma = tma_ring ? 1 : 0;
   // single instance, PDL finalize: it starts on the finished-unit count
   const bool early = pl.hmode && pl.spi > 1 && pl.instances == 1 && !ctx->prof_after;
   p.arrive = early ? ctx->arrive : nullptr;
@@ -553,14 +549,11 @@ int build_host(hood_ctx* ctx, const S* h_pts, long long n, long long block_len, 
   CUtensorMap map;
   long long full_rows = 0;
   std::memset(&map, 0, sizeof(map));
-  const bool tma_ring = pl.hmode && ring_tma() && !(flags & HOOD_FLAG_CHECK_TRIPLES);
   if (!pl.hmode && (rc = encode_map<S>(d_in, n, pl.rows, &map, &full_rows))) return rc;
-  if (tma_ring && (rc = encode_map<S>(d_in, n, 32, &map, &full_rows))) return rc;
   cudaStream_t sc = ctx->s_copy, sk = ctx->s_comp;
   order_after_last(ctx, sk);
   cudaMemsetAsync(ctx->err, 0xff, sizeof(DevError), sk);
   SlabParams<S> p = slab_params<S>(ctx, pl, d_in, d_out, ctx->d_counts, full_rows, flags);
-  p.ring_tma = tma_ring ? 1 : 0;
   const bool full_ok = pl.hmode && pl.spi > 1 && pl.instances == 1;
   p.full_units = full_ok ? ctx->arrive + 1 : nullptr;
   const int chunks = (pl.hmode && pl.instances == 1 && pl.units >= hood_ctx::kChunks) ? hood_ctx::kChunks : 1;

@@ -558,8 +558,7 @@ struct RingLayout {
   // [2] the hood's last two corners after a direct block append; aliases the
   // tree starts (a merge tree clears the cache's validity before it runs)
   static constexpr size_t HT = MNS;
-  static constexpr size_t BAR = up(MNC + 32 * 4, 8);                    // [R] slot mbarriers (TMA ring)
-  static constexpr size_t BYTES = up(BAR + (size_t)R * 8, 16);          // per-warp state
+  static constexpr size_t BYTES = up(MNC + 32 * 4, 16);                 // per-warp state
   static constexpr size_t CTA_BYTES(int warps) { return (size_t)warps * (RINGB + BYTES); }
 };
 
@@ -925,15 +924,11 @@ __device__ __noinline__ AppendRes append_full_block(unsigned a, unsigned slot_ba
 // TRI: the variant with validate_points' consecutive-triple margin check
 // fused into the landing pass (HOOD_FLAG_CHECK_TRIPLES builds only; a call in
 // the landing pass costs the plain kernel registers, so it is compiled apart).
-// TMA: the ring is filled by one cp.async.bulk.tensor (UTMALDG) per block and
-// warp instead of 8 cp.async per lane: lane 0 issues a 4 KB tile (32 rows of
-// 128 B, CU_TENSOR_MAP_SWIZZLE_128B -- the hardware writes exactly the
-// lane-run swizzle of ring_rot) completing on the slot's mbarrier, which the
-// whole warp waits on; warps stay independent.  The input's partial last
-// block (outside the tensor map's full rows) is staged by plain loads.
-template <class S, int D, int P, int U_, bool LEAN = false, bool TRI = false, bool TMA = false>
-__global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG)
-    ring_hull_kernel(const __grid_constant__ CUtensorMap tmap, const SlabParams<S> p) {
+// (A per-warp TMA fill -- one cp.async.bulk.tensor tile per block completing
+// on a slot mbarrier -- was measured against this cp.async ring in round 2 and
+// lost on every large config: profiles/r02/ab_tma.md.)
+template <class S, int D, int P, int U_, bool LEAN = false, bool TRI = false>
+__global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams<S> p) {
   using V = typename PointT<S>::V;
   using L = typename Ld16<S>::T;
   using LY = RingLayout<S, D, P, U_>;
@@ -967,15 +962,6 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG)
   long long* mns = reinterpret_cast<long long*>(wb + LY::MNS);
   int* mnc = reinterpret_cast<int*>(wb + LY::MNC);
   V* htail = reinterpret_cast<V*>(wb + LY::HT);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(wb + LY::BAR);
-  unsigned tma_phase = 0, tma_pend = 0;  // per slot: parity of its next completion / a load in flight
-  if constexpr (TMA) {
-    if (lane == 0) {
-      for (int i = 0; i < R; ++i) mbar_init(&bars[i], 1);
-      fence_barrier_init();
-    }
-    __syncwarp();
-  }
   const V* gpts = reinterpret_cast<const V*>(p.pts);
   const unsigned char* gbytes = reinterpret_cast<const unsigned char*>(p.pts) + lane * 16;
   V* gout = reinterpret_cast<V*>(p.out);
@@ -1022,40 +1008,6 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG)
   auto issue = [&](int b, int s) {
     const long long off = (long long)b * BB;
     const unsigned dst = wr + s * BB;
-    if constexpr (TMA) {
-      __syncwarp();  // every lane is done with the slot's previous contents
-      tma_pend |= 1u << s;
-      if (b < nfull) {
-        if (lane == 0) {
-          fence_proxy_async();  // order the slot's generic writes before the async-proxy fill
-          mbar_expect_tx(&bars[s], (unsigned)BB);
-#if HOOD_L2_EVICT_FIRST
-          tma_load_2d_hint(ring_s + s * BB, &tmap, 0, b * 32, smem_u32(&bars[s]), l2pol);
-#else
-          tma_load_2d_hint(ring_s + s * BB, &tmap, 0, b * 32, smem_u32(&bars[s]), 0ull);
-#endif
-        }
-      } else {
-        // the partial last block: 16-byte pieces that exist, zeros past n
-#pragma unroll
-        for (int j = 0; j < U; ++j) {
-          const long long at = off + lane * 16 + j * 512;
-          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (at + 16 <= n_bytes) v = *reinterpret_cast<const float4*>(reinterpret_cast<const unsigned char*>(p.pts) + at);
-          else if (at < n_bytes) {  // a tail shorter than 16 bytes (one float2)
-            const float2 h = *reinterpret_cast<const float2*>(reinterpret_cast<const unsigned char*>(p.pts) + at);
-            v.x = h.x;
-            v.y = h.y;
-          }
-          const unsigned d = (dst + j * 512) ^ (U == 8 ? (j & 1) << 6 : 0);
-          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(d), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
-                       : "memory");
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bars[s]);
-      }
-      return;
-    }
     if (b < nfull) {
 #pragma unroll
       for (int j = 0; j < U; ++j)
@@ -1194,7 +1146,7 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG)
 #pragma unroll 1
   for (int s = 0; s < D + P; ++s) {
     if (ci.b < ci.e) issue(ci.b, s);
-    if constexpr (!TMA) cp_async_commit();
+    cp_async_commit();
     advance(ci);
   }
   // the first unit's anchors and predecessor x: loaded behind the prologue
@@ -1202,22 +1154,7 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG)
   S pre_l, pre_r;
   ext_partial(cc.b, cc.e, pre_l, pre_r);
   const S pre_x = (cc.b % bpi) != 0 ? gpts[(long long)cc.b * BP - 1].x : NEG;
-  // block k lands in slot s: wait for its fill (TMA: the slot's mbarrier)
-  auto wait_slot = [&](int slot) {
-    if constexpr (TMA) {
-      if (tma_pend & (1u << slot)) {
-        mbar_wait(&bars[slot], (tma_phase >> slot) & 1u);
-        tma_phase ^= 1u << slot;
-        tma_pend &= ~(1u << slot);
-      }
-    }
-  };
-  if constexpr (TMA) {
-#pragma unroll
-    for (int i = 0; i < D; ++i) wait_slot(i);
-  } else {
-    cp_async_wait<P>();
-  }
+  cp_async_wait<P>();
   __syncwarp();
   UnitCur cf = cc;
   bool cf_first = true;  // the next block to land starts its unit
@@ -1293,13 +1230,9 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG)
   while (cc.b < cc.e) {
     // keep P blocks in flight: issue k+D+P, then block k+D has landed
     if (ci.b < ci.e) issue(ci.b, s_new);
+    cp_async_commit();
     advance(ci);
-    if constexpr (TMA) {
-      wait_slot(s_far);
-    } else {
-      cp_async_commit();
-      cp_async_wait<P>();
-    }
+    cp_async_wait<P>();
     __syncwarp();  // the landed block was copied by all lanes
     {
       HOOD_TIC();
@@ -1534,12 +1467,7 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG)
     }
     advance(cc);
   }
-  if constexpr (TMA) {
-#pragma unroll
-    for (int i = 0; i < R; ++i) wait_slot(i);  // no fill may outlive the CTA
-  } else {
-    cp_async_wait<0>();
-  }
+  cp_async_wait<0>();
   if (kTrace && p.trace && lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(p.trace) + 1, gtimer());
   if (kTrace && p.trace && lane == 0) {
     p.trace[1024 + 4 * gw + 1] = (long long)gtimer();
@@ -2672,15 +2600,6 @@ struct DevLaunchState {
 static DevLaunchState g_dev_state[kMaxDevices][2];  // [device][f64]
 static std::mutex g_dev_mu;
 
-// HOOD_RING_TMA=1: the TMA-filled ring (A/B of round 2)
-bool ring_tma() {
-  static const bool on = [] {
-    const char* e = std::getenv("HOOD_RING_TMA");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-
 template <class S>
 static const DevLaunchState& dev_state() {
   int d = 0;
@@ -2700,8 +2619,6 @@ static const DevLaunchState& dev_state() {
     st.inst_occ = occ_of(instance_hull_kernel<S>, inst_smem_bytes<S>(), kThreads);
     occ_of(ring_hull_kernel<S, kRingD, kRingP, kRingU, true, true>, ring_smem<S, true>(), 32 * kRingWarps);
     occ_of(ring_hull_kernel<S, kRingD, kRingP, kRingU, false, true>, ring_smem<S, false>(), 32 * kRingWarps);
-    occ_of(ring_hull_kernel<S, kRingD, kRingP, kRingU, true, false, true>, ring_smem<S, true>(), 32 * kRingWarps);
-    occ_of(ring_hull_kernel<S, kRingD, kRingP, kRingU, false, false, true>, ring_smem<S, false>(), 32 * kRingWarps);
     cudaFuncSetAttribute(finalize_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     st.fin_attr = true;
     st.ring_occ = occ_of(ring_hull_kernel<S, kRingD, kRingP, kRingU, false>, ring_smem<S, false>(),
@@ -2758,16 +2675,12 @@ void launch_slab_kernel(const SlabParams<S>& p, const CUtensorMap* tmap, int gri
   cfg.attrs = at;
   cfg.numAttrs = reset_err ? 1 : 0;
   cfg.dynamicSmemBytes = p.lean ? ring_smem<S, true>() : ring_smem<S, false>();
-  const CUtensorMap& tm = *tmap;
   if (p.check_triples) {
-    if (p.lean) cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kRingU, true, true>, tm, p);
-    else cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kRingU, false, true>, tm, p);
-  } else if (p.ring_tma) {
-    if (p.lean) cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kRingU, true, false, true>, tm, p);
-    else cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kRingU, false, false, true>, tm, p);
+    if (p.lean) cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kRingU, true, true>, p);
+    else cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kRingU, false, true>, p);
   } else {
-    if (p.lean) cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kRingU, true, false>, tm, p);
-    else cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kRingU, false, false>, tm, p);
+    if (p.lean) cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kRingU, true, false>, p);
+    else cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kRingU, false, false>, p);
   }
 }
 

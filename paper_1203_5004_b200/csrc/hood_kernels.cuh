@@ -62,7 +62,6 @@ struct SlabParams {
   long long* trace;         // optional per-tile clock64 trace (profiling)
   long long read_lim;       // points at or past this index may not be read yet (host-path chunks)
   int lean;                 // ring kernel: the register-light variant (batched builds)
-  int ring_tma;             // ring kernel: TMA-filled ring (tmap = the input as rows of 128 B, box 32 rows)
   unsigned* arrive;         // optional: +1 per finished unit (release), read by the finalize
   // optional (single instance): +1 per unit whose hood is ALL its points and
   // whose left seam continues the unit before it concavely (arc-like input);
@@ -140,6 +139,5 @@ int slab_warps_per_cta();      // units (warps) per slab-kernel CTA
 template <class S>
 int slab_tile_rows(bool hmode);  // chunk rows (= threads) per tile
 size_t finalize_smem(int fcap_bytes, int slabs);
-bool ring_tma();                // HOOD_RING_TMA=1: the ring kernel fills its ring with TMA
 
 }  // namespace hood_b200

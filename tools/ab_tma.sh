@@ -1,3 +1,4 @@
+# (Needs the commit that added HOOD_RING_TMA; the variant was removed after this A/B.)
 # A/B of the ring kernel's fill: 8 cp.async (LDGSTS) per lane vs one TMA tile
 # (UTMALDG + mbarrier) per warp and block; same box, alternating, 3 rounds.
 mkdir -p gpurun_out
