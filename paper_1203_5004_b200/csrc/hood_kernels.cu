@@ -625,6 +625,11 @@ __device__ __forceinline__ float2 lds_pt(unsigned a, float2*) {
 }
 __device__ __forceinline__ double2 lds_pt(unsigned a, double2*) { return lds16<double2>(a); }
 
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+
 // Survivors of a block at an instance edge (lane bit i: point i of the lane's
 // run, smem run address a, first global index q0): exact per-point anchors
 // on the side(s) without a block anchor -- left = max y of everything before
@@ -642,8 +647,9 @@ __device__ __noinline__ unsigned edge_survivors(unsigned a, long long q0, long l
   // keep the 16-byte loads whole (no narrowed, bank-conflicting y loads):
   // y + 0 * x is y exactly for finite x (x is validated finite and ordered;
   // a non-finite x is an x error whatever this returns), and IEEE forbids
-  // folding 0 * x, so the x components stay live
-  auto keep_width = [](const typename PointT<S>::V& q) -> S { return q.y + (S)0 * q.x; };
+  // folding 0 * x, so the x components stay live; separately rounded
+  // intrinsics, so it never becomes an FMA (the kernels carry no DFMA)
+  auto keep_width = [](const typename PointT<S>::V& q) -> S { return add_rn(q.y, mul_rn((S)0, q.x)); };
   S yv[NP];
   S t = NEG;
   if (q0 + NP <= n) {  // the lane's whole run exists (every block but the input's last)
