@@ -579,7 +579,10 @@ int build_host(hood_ctx* ctx, const S* h_pts, long long n, long long block_len, 
     launch_slab_kernel<S>(p, &map, (int)std::min<long long>((units_c + per_cta - 1) / per_cta, pl.grid), sk);
   };
   const size_t bytes = (size_t)n * sizeof(V);
-  if (is_pinned(h_pts)) {
+  // small pageable inputs (at most two staging chunks) go through the
+  // driver's own staging: spawning the copy threads would cost more
+  const bool small = bytes <= 2 * (ctx->stager ? ctx->stager->chunk : (size_t)(8u << 20));
+  if (small || is_pinned(h_pts)) {
     for (int c = 0; c < chunks; ++c) {
       long long u0, u1, p0, p1;
       range_of(c, u0, u1, p0, p1);
