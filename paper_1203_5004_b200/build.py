@@ -51,6 +51,21 @@ def build(verbose: bool = False, force: bool = False) -> str:
     return SO
 
 
+def build_checked(force: bool = False) -> str:
+    """Bounds-checked build (-DHOOD_CHECKED: device-side invariant checks that
+    trap), as lib/libhood_b200_checked.so; the GPU suite runs against it with
+    HOOD_B200_LIB pointing at it (compute-sanitizer is closed on the pool)."""
+    os.makedirs(LIB, exist_ok=True)
+    so = os.path.join(LIB, "libhood_b200_checked.so")
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "hood_b200.h")]
+    if force or _stale(so, deps):
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-shared",
+               "--expt-relaxed-constexpr", "-DHOOD_CHECKED", "-I", os.path.join(ROOT, "include"), "-o", so]
+        cmd += [os.path.join(CSRC, f) for f in SOURCES]
+        subprocess.run(cmd, check=True)
+    return so
+
+
 def build_trace(force: bool = False) -> str:
     """Profiling build (tools/trace_ring.py, tools/trace_finalize.py): the same
     sources with -DHOOD_TRACE (in-kernel globaltimer/clock64 stamps), as
@@ -70,6 +85,9 @@ def build_trace(force: bool = False) -> str:
 if __name__ == "__main__":
     if "--trace" in sys.argv:
         print(build_trace(force="--force" in sys.argv))
+        sys.exit(0)
+    if "--checked" in sys.argv:
+        print(build_checked(force="--force" in sys.argv))
         sys.exit(0)
     build(verbose="--verbose" in sys.argv, force="--force" in sys.argv)
     print(SO)

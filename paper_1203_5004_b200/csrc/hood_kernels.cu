@@ -42,6 +42,25 @@ constexpr bool kTrace = true;
 constexpr bool kTrace = false;
 #endif
 
+// Bounds/invariant checks, compiled in only with -DHOOD_CHECKED (the checked
+// build, lib/libhood_b200_checked.so: compute-sanitizer is closed on the GPU
+// pool, so the GPU suite runs against this build instead).  A violation
+// prints the site and traps, failing the launch.
+#ifdef HOOD_CHECKED
+#define HOOD_CHECK(cond)                                                                        \
+  do {                                                                                          \
+    if (!(cond)) {                                                                              \
+      printf("HOOD_CHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                                \
+      __trap();                                                                                 \
+    }                                                                                           \
+  } while (0)
+#else
+#define HOOD_CHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 template <class S> struct HCap { static constexpr int value = 128; };  // running hood kept in smem (corners)
 
 
@@ -358,6 +377,7 @@ __device__ __noinline__ HoodState merge_block_lean(typename PointT<S>::V* SB, in
           h.in_smem = 0;
         }
         V* dstp = h.in_smem ? Hs : gslab;
+        HOOD_CHECK(!h.in_smem || h.n + m <= HC);
         for (int i = lane; i < m; i += 32) dstp[h.n + i] = SB[i];
         __syncwarp();
         h.n += m;
@@ -464,6 +484,7 @@ __device__ __noinline__ HoodState merge_block_tree(typename PointT<S>::V* SB, in
           h.in_smem = 0;
         }
         V* dstp = h.in_smem ? Hs : gslab;
+        HOOD_CHECK(!h.in_smem || h.n + m <= HC);
         for (int i = lane; i < m; i += 32) dstp[h.n + i] = SB[i];
         __syncwarp();
         h.n += m;
@@ -492,6 +513,7 @@ __device__ __noinline__ HoodState merge_block_tree(typename PointT<S>::V* SB, in
     h.in_smem = 0;
   }
   V* dstp = h.in_smem ? Hs : gslab;
+  HOOD_CHECK(!h.in_smem || newN <= HC);
   for (long long i = lane; i < kq - qidx; i += 32) dstp[pidx + 1 + i] = SB[qs + qidx + i];
   __syncwarp();
   h.n = newN;
@@ -1293,6 +1315,7 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
           sv = (bs + cl * NP + lane < n) && !(q.y < tau);
         }
         const unsigned sm = __ballot_sync(FULL, sv);
+        HOOD_CHECK(pend + __popc(sm) <= PC);
         if (sv) PBf[pend + __popc(sm & below)] = q;  // room: pend <= PC - 2 NP here
         pend += __popc(sm);
       }
@@ -1361,6 +1384,7 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
         for (int i = 0; i < NP; ++i)
           if ((svm >> i) & 1u) dst[pos++] = pt_of(c[i / PPL], i % PPL);
       } else {
+        HOOD_CHECK(pend + total <= PC);
         // few: the lane's survivors straight from the slot, one per set bit
         for (unsigned m = svm; m; m &= m - 1) {
           const int i = __ffs(m) - 1;
@@ -1406,6 +1430,8 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
       } else {
         flush();
       }
+      HOOD_CHECK(hs.n <= min(n, (long long)(cc.b + 1) * BP) - ubase);  // a hood is a subset of its unit
+      HOOD_CHECK(!hs.in_smem || hs.n <= HC);
       if (hs.in_smem && !written)
         for (long long e = lane; e < hs.n; e += 32) gout[ubase + e] = Hs[e];
       if (spi > 1) {
@@ -2038,6 +2064,7 @@ __device__ __noinline__ void finalize_body(const FinalizeParams<S> p) {
               oc = o2;
             }
           }
+          HOOD_CHECK(i >= A || (c < C && i - oc >= 0 && i - oc < CAP));
           if (i < A) Hd[i] = stg[c * CAP + (i - oc)];
         }
         __syncwarp();
