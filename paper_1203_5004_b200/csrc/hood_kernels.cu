@@ -559,22 +559,35 @@ __device__ __forceinline__ void cp_async_wait() {
 // Per-warp shared memory of the ring kernel: R = D + P + 1 block slots (the
 // block being processed, D landed blocks of lookahead, P blocks in flight),
 // the unit's running hood and a small buffer of pending survivors.
-template <class S, int D, int P, int U_>
+#ifndef HOOD_LEAN_HC
+#define HOOD_LEAN_HC 128
+#endif
+#ifndef HOOD_HC
+#define HOOD_HC 128
+#endif
+#ifndef HOOD_PC
+#define HOOD_PC 64
+#endif
+#ifndef HOOD_LEAN_PC
+#define HOOD_LEAN_PC 64
+#endif
+template <class S, int D, int P, int U_, bool LEAN = false>
 struct RingLayout {
   using V = typename PointT<S>::V;
+  static constexpr int HC = LEAN ? HOOD_LEAN_HC : HOOD_HC;              // running hood kept in smem (corners)
   static constexpr size_t up(size_t x, size_t a) { return (x + a - 1) / a * a; }
   static constexpr int U = U_;                                          // 16-byte chunks per lane per block
   static constexpr int R = D + P + 1;                                   // ring slots
   static constexpr int BP = 32 * U * Ld16<S>::PPL;                      // points per block
   static constexpr size_t BB = 32 * U * 16;                             // bytes per block
-  static constexpr int PC = 64;                                         // pending survivor capacity
+  static constexpr int PC = LEAN ? HOOD_LEAN_PC : HOOD_PC;              // pending survivor capacity
   // The CTA's rings come first, warp w's at w * RINGB: every slot starts on a
   // 1024-byte boundary (the 128B-swizzle atom of a TMA tile, whose row r of
   // 128 bytes holds its 16-byte unit u at u ^ (r & 7) -- exactly the lane-run
   // swizzle of ring_rot).  Then each warp's own state:
   static constexpr size_t RINGB = (size_t)R * BB;
   static constexpr size_t HS = 0;                                       // [HC] running unit hood
-  static constexpr size_t PB = HS + (size_t)HCap<S>::value * sizeof(V); // [PC] pending survivors
+  static constexpr size_t PB = HS + (size_t)HC * sizeof(V);             // [PC] pending survivors
   static constexpr size_t MNS = up(PB + (size_t)PC * sizeof(V), 8);     // [32] tree starts
   static constexpr size_t MNC = MNS + 32 * 8;                           // [32] tree counts
   // [2] the hood's last two corners after a direct block append; aliases the
@@ -959,12 +972,12 @@ template <class S, int D, int P, int U_, bool LEAN = false, bool TRI = false>
 __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams<S> p) {
   using V = typename PointT<S>::V;
   using L = typename Ld16<S>::T;
-  using LY = RingLayout<S, D, P, U_>;
+  using LY = RingLayout<S, D, P, U_, LEAN>;
   constexpr int U = LY::U, R = LY::R, PPL = Ld16<S>::PPL;
   constexpr int NP = U * PPL;  // points per lane run
   constexpr int BP = LY::BP;
   constexpr int BB = (int)LY::BB;
-  constexpr int HC = HCap<S>::value;
+  constexpr int HC = LY::HC;
   constexpr int PC = LY::PC;
   constexpr int EXT = 512;
   constexpr unsigned FULL = 0xffffffffu;
@@ -1490,10 +1503,10 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
             if (ok) atomicAdd(p.full_units, 1u);
           }
         }
-        if (p.arrive && lane == 0) {  // the unit's hood, count and anchor are published
-          __threadfence();  // cumulative: covers the lanes' writes ordered by the __syncwarp
-          atomicAdd(p.arrive, 1u);
-        }
+      }
+      if (p.arrive && lane == 0) {  // the unit's hood, count and anchor are published
+        __threadfence();  // cumulative: covers the lanes' writes ordered by the __syncwarp
+        atomicAdd(p.arrive, 1u);
       }
       fresh = true;
     }
@@ -2618,7 +2631,7 @@ constexpr int kRingD = 1, kRingP = 1, kRingU = 8;
 
 template <class S, bool LEAN>
 static size_t ring_smem() {
-  return RingLayout<S, kRingD, kRingP, kRingU>::CTA_BYTES(kRingWarps);
+  return RingLayout<S, kRingD, kRingP, kRingU, LEAN>::CTA_BYTES(kRingWarps);
 }
 
 // Per-device launch state: the dynamic shared-memory opt-in
