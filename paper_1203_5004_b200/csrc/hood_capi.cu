@@ -39,6 +39,11 @@ struct hood_ctx {
   void* seg_apt = nullptr;  // double2-sized slots (fits float2 too)
   long long* seg_base = nullptr;
   long long seg_cap = 0;
+  unsigned long long* steal_w = nullptr;  // per unit claim word (0xff.. = not stealable)
+  int* steal_done = nullptr;              // per unit parts done (0 between builds)
+  int* part_cnt = nullptr;                // per part (2 per unit)
+  long long* part_base = nullptr;
+  unsigned steal_epoch = 0;
   DevError* err = nullptr;
   unsigned* arrive = nullptr;  // finished-unit counter (ring kernel -> finalize), zero between builds
   void* warm = nullptr;        // the finalize's warm-up instance (kWarmBytes)
@@ -150,9 +155,10 @@ int ensure_ws(hood_ctx* ctx, long long slabs) {
     if (cudaMalloc(&ctx->err, sizeof(DevError)) != cudaSuccess) return HOOD_ERR_CUDA;
     if (cudaMalloc(&ctx->done, sizeof(int)) != cudaSuccess) return HOOD_ERR_CUDA;
     if (cudaMemset(ctx->err, 0xff, sizeof(DevError)) != cudaSuccess) return HOOD_ERR_CUDA;
-    // [0] finished units, [1] full units (both zeroed by the finalize that reads them)
-    if (cudaMalloc(&ctx->arrive, 2 * sizeof(unsigned)) != cudaSuccess) return HOOD_ERR_CUDA;
-    if (cudaMemset(ctx->arrive, 0, 2 * sizeof(unsigned)) != cudaSuccess) return HOOD_ERR_CUDA;
+    // [0] finished units, [1] full units (both zeroed by the finalize that
+    // reads them), [2] steals so far (hood_internal_steals reads and zeroes it)
+    if (cudaMalloc(&ctx->arrive, 4 * sizeof(unsigned)) != cudaSuccess) return HOOD_ERR_CUDA;
+    if (cudaMemset(ctx->arrive, 0, 4 * sizeof(unsigned)) != cudaSuccess) return HOOD_ERR_CUDA;
     if (cudaMalloc(&ctx->warm, kWarmBytes) != cudaSuccess) return HOOD_ERR_CUDA;
     // zero counts until the first reset kernel writes the instance (same
     // bytes every build, so a finalize never reads a torn one)
@@ -162,10 +168,24 @@ int ensure_ws(hood_ctx* ctx, long long slabs) {
     cudaFree(ctx->seg_cnt);
     cudaFree(ctx->seg_apt);
     cudaFree(ctx->seg_base);
+    cudaFree(ctx->steal_w);
+    cudaFree(ctx->steal_done);
+    cudaFree(ctx->part_cnt);
+    cudaFree(ctx->part_base);
     const long long cap = std::max(slabs, 4096LL);
     if (cudaMalloc(&ctx->seg_cnt, cap * sizeof(int)) != cudaSuccess ||
         cudaMalloc(&ctx->seg_apt, cap * 2 * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&ctx->seg_base, cap * sizeof(long long)) != cudaSuccess)
+        cudaMalloc(&ctx->seg_base, cap * sizeof(long long)) != cudaSuccess ||
+        cudaMalloc(&ctx->steal_w, cap * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&ctx->steal_done, cap * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&ctx->part_cnt, 2 * cap * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&ctx->part_base, 2 * cap * sizeof(long long)) != cudaSuccess)
+      return HOOD_ERR_CUDA;
+    // claim words start "not stealable" (a stolen count != 0); every owner
+    // resets its own word at the start of each build, and every build leaves
+    // every word in a state no thief takes (fully claimed, or stolen once)
+    if (cudaMemset(ctx->steal_w, 0xff, cap * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMemset(ctx->steal_done, 0, cap * sizeof(int)) != cudaSuccess)
       return HOOD_ERR_CUDA;
     ctx->seg_cap = cap;
   }
@@ -189,6 +209,9 @@ int encode_map(const void* pts, long long n, int box_rows, CUtensorMap* map, lon
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? HOOD_OK : HOOD_ERR_CUDA;
 }
+
+bool steal_enabled();
+constexpr long long kStealMinUnitBlocks = 64;
 
 template <class S>
 SlabParams<S> slab_params(hood_ctx* ctx, const Plan& pl, const void* pts, void* corners, int* counts,
@@ -215,6 +238,18 @@ SlabParams<S> slab_params(hood_ctx* ctx, const Plan& pl, const void* pts, void* 
   p.seg_cnt = ctx->seg_cnt;
   p.seg_apt = ctx->seg_apt;
   p.seg_base = ctx->seg_base;
+  // tail stealing pays only on long units (config 4: ~590 blocks per unit;
+  // on 9-18-block units it costs ~10%: profiles/r02/ab_steal.md)
+  const bool long_units = pl.spi > 1 && pl.tpi / pl.spi >= kStealMinUnitBlocks;
+  if (pl.hmode && long_units && !pl.lean && !(flags & HOOD_FLAG_CHECK_TRIPLES) && steal_enabled()) {
+    ctx->steal_epoch = (ctx->steal_epoch + 1) % 0xffffu;  // 0xffff: the memset state, never an epoch
+    p.steal_epoch = ctx->steal_epoch;
+    p.steal_w = ctx->steal_w;
+    p.steal_count = ctx->arrive + 2;
+    p.steal_done = ctx->steal_done;
+    p.part_cnt = ctx->part_cnt;
+    p.part_base = ctx->part_base;
+  }
   p.err = ctx->err;
   p.check_range = (flags & HOOD_FLAG_CHECK_RANGE) ? 1 : 0;
   p.check_triples = (flags & HOOD_FLAG_CHECK_TRIPLES) ? 1 : 0;
@@ -262,6 +297,15 @@ void record_event(cudaEvent_t ev, cudaStream_t st) {
 }
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// HOOD_STEAL=0 turns tail stealing off (A/B and diagnosis only).
+bool steal_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HOOD_STEAL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 bool capturing(cudaStream_t st) {
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -959,6 +1003,10 @@ int hood_destroy(hood_ctx* c) {
   cudaFree(c->seg_cnt);
   cudaFree(c->seg_apt);
   cudaFree(c->seg_base);
+  cudaFree(c->steal_w);
+  cudaFree(c->steal_done);
+  cudaFree(c->part_cnt);
+  cudaFree(c->part_base);
   cudaFree(c->err);
   cudaFree(c->done);
   cudaFree(c->arrive);
@@ -1037,6 +1085,17 @@ extern "C" int hood_internal_set_debug(hood_ctx* ctx, int mode, void* trace) {
   ctx->dbg = mode;
   ctx->trace = reinterpret_cast<long long*>(trace);
   return HOOD_OK;
+}
+
+// Tests / diagnosis: the number of tail steals since the last call (synchronizes).
+extern "C" long long hood_internal_steals(hood_ctx* ctx) {
+  if (!ctx || !ctx->arrive) return -1;
+  cudaSetDevice(ctx->device);
+  if (ctx->have_last) cudaStreamSynchronize(ctx->last_stream);
+  unsigned v = 0;
+  if (cudaMemcpy(&v, ctx->arrive + 2, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  cudaMemset(ctx->arrive + 2, 0, sizeof(unsigned));
+  return v;
 }
 
 // Measurement only: one bare read of [p, p + bytes) (bench.py's attainable

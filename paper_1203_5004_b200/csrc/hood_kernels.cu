@@ -593,7 +593,12 @@ struct RingLayout {
   // [2] the hood's last two corners after a direct block append; aliases the
   // tree starts (a merge tree clears the cache's validity before it runs)
   static constexpr size_t HT = MNS;
-  static constexpr size_t BYTES = up(MNC + 32 * 4, 16);                 // per-warp state
+  // STEAL: the ranges the issue cursor hands to the landing / processing
+  // cursors (4 entries: first block, known end, unit, flags, unit end) and the
+  // owner's claim state
+  static constexpr int QN = 4;
+  static constexpr size_t Q = up(MNC + 32 * 4, 16);
+  static constexpr size_t BYTES = up(Q + (LEAN ? 0 : (size_t)QN * 5 * 4 + 16), 16);  // per-warp state
   static constexpr size_t CTA_BYTES(int warps) { return (size_t)warps * (RINGB + BYTES); }
 };
 
@@ -861,6 +866,48 @@ __device__ __forceinline__ int ring_rot(int l) {
   return U == 8 ? (l & 7) : ((l >> 1) & 3);
 }
 
+// Loads that bypass L1 (ld.global.cg): another SM's writes, published with
+// a fence + atomic, are read from L2.
+template <class V>
+struct CgAcc {
+  V* p;
+  __device__ __forceinline__ V ld(long long i) const { return __ldcg(p + i); }
+  __device__ __forceinline__ void st(long long i, V v) const { p[i] = v; }
+};
+
+struct Merged {
+  long long n, base;
+};
+
+// STEAL: the two parts of a stolen unit -- P (the owner's, left) at bP and Q
+// (the thief's tail) at bQ, each a strict upper hood in its output slots --
+// merged into one: the common tangent by bridge() (the g/f classifiers as
+// monotone searches, kernel.hpp:31-67), then the splice P[..pidx] ++ Q[qidx..]
+// (kernel.cpp:117-137) in place at bP (a forward copy: the destination is
+// never right of the source).
+template <class V>
+__device__ __noinline__ Merged merge_parts(V* g, long long bP, long long cP, long long bQ, long long cQ) {
+  const int lane = threadIdx.x & 31;
+  if (cQ == 0) return Merged{cP, bP};
+  if (cP == 0) return Merged{cQ, bQ};
+  long long pidx = 0, qidx = 0;
+  if (lane == 0) bridge<V>(CgAcc<V>{g}, bP, cP, CgAcc<V>{g}, bQ, cQ, pidx, qidx);
+  pidx = __shfl_sync(0xffffffffu, pidx, 0);
+  qidx = __shfl_sync(0xffffffffu, qidx, 0);
+  const long long len = cQ - qidx, dst = bP + pidx + 1, src = bQ + qidx;
+  if (dst != src) {
+    for (long long e0 = 0; e0 < len; e0 += 32) {
+      const long long e = e0 + lane;
+      V v{};
+      if (e < len) v = __ldcg(g + src + e);
+      __syncwarp();
+      if (e < len) g[dst + e] = v;
+      __syncwarp();
+    }
+  }
+  return Merged{pidx + 1 + len, bP};
+}
+
 struct AppendRes {
   HoodState h;
   bool ok;
@@ -968,7 +1015,13 @@ __device__ __noinline__ AppendRes append_full_block(unsigned a, unsigned slot_ba
 // (A per-warp TMA fill -- one cp.async.bulk.tensor tile per block completing
 // on a slot mbarrier -- was measured against this cp.async ring in round 2 and
 // lost on every large config: profiles/r02/ab_tma.md.)
-template <class S, int D, int P, int U_, bool LEAN = false, bool TRI = false>
+// STEAL: multi-unit instances balance their tails: each warp claims its
+// unit's blocks from the front in pairs (one claim in flight), and a warp whose
+// work is done steals the back half of the unit with the most unclaimed blocks
+// (one CAS on the unit's claim word; one steal per unit).  The two parts of a
+// stolen unit are merged by the later of them (bridge + splice) into the
+// unit's one segment, so the finalize is unchanged.
+template <class S, int D, int P, int U_, bool LEAN = false, bool TRI = false, bool STEAL = false>
 __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams<S> p) {
   using V = typename PointT<S>::V;
   using L = typename Ld16<S>::T;
@@ -1041,6 +1094,169 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
     }
     return false;
   };
+  // ---- STEAL: the issue cursor's ranges (queue in smem, read by the landing
+  // and processing cursors), the owner's claims, the steals
+  int* qb = reinterpret_cast<int*>(wb + LY::Q);  // [QN] first block of the range
+  int* qe = qb + LY::QN;                         // [QN] its known end (grows while the owner claims)
+  int* qu = qe + LY::QN;                         // [QN] its unit
+  int* qf = qu + LY::QN;                         // [QN] 1: a stolen tail, 2: an owner range stolen from
+  int* qx = qf + LY::QN;                         // [QN] the unit's end block (edge anchors)
+#ifndef HOOD_STEAL_G
+#define HOOD_STEAL_G 8
+#endif
+#ifndef HOOD_STEAL_MIN
+#define HOOD_STEAL_MIN 8
+#endif
+  constexpr int kG = HOOD_STEAL_G;            // blocks per owner claim (the next claim is in flight a whole claim ahead)
+  constexpr int kMinSteal = HOOD_STEAL_MIN;   // smallest stolen tail (blocks)
+  int ci_r = 0;                 // range number of the issue cursor
+  int ci_mode = 0;              // 0 owner, 1 search, 2 stolen range, 3 done
+  int ci_b = 0;                 // next block to issue
+  int claimed_to = 0;           // owner: end of its claimed blocks
+  // cold state in smem (touched once per claim or range): [0] a claim in
+  // flight, [1] blocks stolen from the owner's unit, [2] the stolen range's end
+  int* cs = qx + LY::QN;
+  // the owner's unit: qb[0] .. qx[0] (queue slot 0 holds range 0 while the owner claims)
+  const long long own_u = p.unit_lo + gw;
+  unsigned long long own_pend = 0;  // lane 0: the claim in flight
+  auto unit_range = [&](long long v, int& b0, int& b1) {
+    const int uu = (int)v, inst = uu / spi, js = uu - inst * spi;
+    b0 = inst * bpi + (int)(((long long)js * bpi) / spi);
+    b1 = inst * bpi + (int)(((long long)(js + 1) * bpi) / spi);
+  };
+  // the back half of the unit with the most unclaimed blocks among 32
+  // sampled units (all of them when there are at most 32), one CAS; one L2
+  // round trip per attempt, attempts repeated only when the CAS loses a race
+  auto steal = [&](int& sb, int& se, int& sv) -> bool {
+    const long long units = p.unit_hi - p.unit_lo;
+    for (int attempt = 0; attempt < 4; ++attempt) {
+      long long best = 0;
+      int bvu = -1;
+      unsigned long long bold = 0;
+      {
+        const unsigned h = ((unsigned)gw * 131u + (unsigned)attempt * 977u + (unsigned)lane * 61u) * 2654435761u;
+        const long long vv = units <= 32 ? (long long)lane : (long long)((h >> 7) % (unsigned)units);
+        const unsigned long long w =
+            vv < units ? *reinterpret_cast<volatile unsigned long long*>(p.steal_w + p.unit_lo + vv) : ~0ull;
+        if ((w >> 32) == ((unsigned long long)p.steal_epoch << 16)) {  // this build's, nothing stolen
+          const long long v = p.unit_lo + vv;
+          int b0, b1;
+          unit_range(v, b0, b1);
+          const long long rem = (long long)(b1 - b0) - (long long)(unsigned)w;
+          if (rem > best) {
+            best = rem;
+            bvu = (int)v;
+            bold = w;
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {  // the same (best, unit) on every lane
+        const long long ob = __shfl_xor_sync(FULL, best, o);
+        const int ov = __shfl_xor_sync(FULL, bvu, o);
+        const unsigned long long oo = __shfl_xor_sync(FULL, bold, o);
+        if (ob > best || (ob == best && ov > bvu)) {
+          best = ob;
+          bvu = ov;
+          bold = oo;
+        }
+      }
+      if (best < 2 * kMinSteal) return false;
+      const int K = (int)min(best / 2, 0xffffLL);
+      unsigned long long got = 0;
+      if (lane == 0) got = atomicCAS(p.steal_w + bvu, bold, bold + ((unsigned long long)K << 32));
+      got = __shfl_sync(FULL, got, 0);
+      if (got == bold) {
+        if (lane == 0 && p.steal_count) atomicAdd(p.steal_count, 1u);
+        int b0, b1;
+        unit_range(bvu, b0, b1);
+        sb = b1 - K;
+        se = b1;
+        sv = bvu;
+        return true;
+      }
+    }
+    return false;
+  };
+  // the next block of the warp's sequence (-1: none); records new ranges
+  auto ci_next = [&]() -> int {
+    for (;;) {
+      if (ci_mode == 0) {
+        if (ci_b < claimed_to) return ci_b;
+        const int own_b0 = qb[0], own_b1 = qx[0];
+        if (cs[0]) {  // consume the claim in flight
+          const unsigned long long pv = __shfl_sync(FULL, own_pend, 0);
+          const int f = (int)(unsigned)pv;
+          const int own_s = (int)((pv >> 32) & 0xffffu);
+          const int cnt = max(0, min(kG, (own_b1 - own_s) - (own_b0 + f)));
+          __syncwarp();
+          if (lane == 0) {
+            cs[0] = 0;
+            cs[1] = own_s;
+          }
+          if (cnt > 0) {
+            claimed_to = own_b0 + f + cnt;
+            if (claimed_to < own_b1 - own_s && lane == 0) {
+              own_pend = atomicAdd(p.steal_w + own_u, (unsigned long long)kG);
+              cs[0] = 1;
+            }
+            if (lane == 0) qe[ci_r & 3] = claimed_to;
+            __syncwarp();
+            continue;
+          }
+        }
+        if (lane == 0 && cs[1]) qf[ci_r & 3] |= 2;  // the owner's range ends; it was stolen from
+        __syncwarp();
+        ci_mode = 1;
+      }
+      if (ci_mode == 1) {
+        int sb, se, sv;
+        if (steal(sb, se, sv)) {
+          ++ci_r;
+          if (lane == 0) {
+            const int j = ci_r & 3;
+            qb[j] = sb;
+            qe[j] = se;
+            qu[j] = sv;
+            qf[j] = 1;
+            qx[j] = se;
+            cs[2] = se;
+          }
+          __syncwarp();
+          ci_b = sb;
+          ci_mode = 2;
+          return ci_b;
+        }
+        ci_mode = 3;
+      }
+      if (ci_mode == 2) {
+        if (ci_b < cs[2]) return ci_b;
+        ci_mode = 1;
+        continue;
+      }
+      return -1;
+    }
+  };
+  // landing / processing cursors over the queue: c.r = range number, c.b =
+  // block, c.e = the range's end as last read (re-read only on reaching it:
+  // an owner's range grows while it claims)
+  auto svalid = [&](const UnitCur& c) -> bool { return c.r <= ci_r && c.b < c.e; };
+  auto sadv = [&](UnitCur& c) -> bool {  // true when it moved into a new range
+    if (c.r > ci_r) return false;
+    ++c.b;
+    if (c.b < c.e) return false;
+    c.e = qe[c.r & 3];
+    if (c.b < c.e) return false;
+    ++c.r;
+    if (c.r <= ci_r) {
+      c.b = qb[c.r & 3];
+      c.e = qe[c.r & 3];
+    } else {
+      c.b = c.e = 0;
+    }
+    return true;
+  };
+
   // copy global block b into ring slot s; the input's last block is clamped
   // (cp.async zero-fills the rest)
 #if HOOD_L2_EVICT_FIRST
@@ -1149,8 +1365,37 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
 #define HOOD_TOC(acc)
 #endif
   UnitCur cc{0, 0, 0};
-  seek(cc);
-  if (!(cc.b < cc.e)) return;
+  if constexpr (STEAL) {
+    if (own_u >= p.unit_hi) return;
+    int own_b0, own_b1;
+    unit_range(own_u, own_b0, own_b1);
+    // the first pair of blocks is the owner's without a claim; the next
+    // claim goes out at once
+    claimed_to = min(own_b0 + kG, own_b1);
+    if (lane == 0) {
+      // this build's epoch, nothing stolen, the first pair claimed
+      p.steal_w[own_u] = ((unsigned long long)p.steal_epoch << 48) | (unsigned long long)(claimed_to - own_b0);
+      if (claimed_to < own_b1) own_pend = atomicAdd(p.steal_w + own_u, (unsigned long long)kG);
+      qb[0] = own_b0;
+      qe[0] = claimed_to;
+      qu[0] = (int)own_u;
+      qf[0] = 0;
+      qx[0] = own_b1;
+      cs[0] = claimed_to < own_b1;
+      cs[1] = 0;
+    }
+    __syncwarp();
+    if ((p.dbg & 4) && (gw & 1)) {  // tests: a slow half of the warps, so the others steal
+      const unsigned long long t0 = gtimer();
+      while (gtimer() - t0 < 300000ull) __nanosleep(1000);
+    }
+    ci_b = own_b0;
+    cc.b = own_b0;
+    cc.e = claimed_to;
+  } else {
+    seek(cc);
+    if (!(cc.b < cc.e)) return;
+  }
 
   // lane partial maxima of the edge anchors of the unit [b, e): up to EXT
   // input points on each side of it inside its instance
@@ -1186,14 +1431,22 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
   UnitCur ci = cc;
 #pragma unroll 1
   for (int s = 0; s < D + P; ++s) {
-    if (ci.b < ci.e) issue(ci.b, s);
+    if constexpr (STEAL) {
+      const int b = ci_next();
+      if (b >= 0) {
+        issue(b, s);
+        ++ci_b;
+      }
+    } else {
+      if (ci.b < ci.e) issue(ci.b, s);
+    }
     cp_async_commit();
-    advance(ci);
+    if constexpr (!STEAL) advance(ci);
   }
   // the first unit's anchors and predecessor x: loaded behind the prologue
   // copies, consumed after they land
   S pre_l, pre_r;
-  ext_partial(cc.b, cc.e, pre_l, pre_r);
+  ext_partial(cc.b, STEAL ? qx[0] : cc.e, pre_l, pre_r);
   const S pre_x = (cc.b % bpi) != 0 ? gpts[(long long)cc.b * BP - 1].x : NEG;
   cp_async_wait<P>();
   __syncwarp();
@@ -1203,7 +1456,7 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
   S lmw[D], win[D];      // lane run / block maxima of sequence blocks k+1 .. k+D
   S lmc, wcur;           // ... of block k
   auto land_next = [&](int slot, S& lm, S& bm) {
-    if (cf.b < cf.e) {
+    if (STEAL ? svalid(cf) : cf.b < cf.e) {
       bool hp = true;
       if (cf_first) {
         hp = (cf.b % bpi) != 0;
@@ -1215,13 +1468,15 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
       lm = NEG;
       bm = NEG;
     }
-    cf_first = advance(cf);
+    if constexpr (STEAL) cf_first = sadv(cf);
+    else cf_first = advance(cf);
   };
   {  // the first block: its predecessor x was loaded up front
     xcf = pre_x;
     lmc = land(cf.b, 0, (cf.b % bpi) != 0, xcf);
     wcur = warp_max_fast(lmc);
-    cf_first = advance(cf);
+    if constexpr (STEAL) cf_first = sadv(cf);
+    else cf_first = advance(cf);
   }
 #pragma unroll
   for (int i = 0; i + 1 < D; ++i) land_next(i + 1, lmw[i], win[i]);
@@ -1268,11 +1523,19 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
   };
 
 #pragma unroll 1
-  while (cc.b < cc.e) {
+  while (STEAL ? svalid(cc) : cc.b < cc.e) {
     // keep P blocks in flight: issue k+D+P, then block k+D has landed
-    if (ci.b < ci.e) issue(ci.b, s_new);
+    if constexpr (STEAL) {
+      const int b = (ci_mode == 0 && ci_b < claimed_to) ? ci_b : ci_next();
+      if (b >= 0) {
+        issue(b, s_new);
+        ++ci_b;
+      }
+    } else {
+      if (ci.b < ci.e) issue(ci.b, s_new);
+    }
     cp_async_commit();
-    advance(ci);
+    if constexpr (!STEAL) advance(ci);
     cp_async_wait<P>();
     __syncwarp();  // the landed block was copied by all lanes
     {
@@ -1283,7 +1546,8 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
 
     if (fresh) {
       fresh = false;
-      u = p.unit_lo + gw + (long long)cc.r * nwarps;
+      if constexpr (STEAL) u = qu[cc.r & 3];
+      else u = p.unit_lo + gw + (long long)cc.r * nwarps;
       inst = spi == 1 ? (int)u : (int)u / spi;
       ubase = (long long)cc.b * BP;
       // edge anchors: max y of up to EXT points on each side of the unit
@@ -1291,7 +1555,7 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
       if (spi == 1) {
         ext_l = ext_r = NEG;
       } else {
-        if (cc.r != 0) ext_partial(cc.b, cc.e, pre_l, pre_r);
+        if (cc.r != 0) ext_partial(cc.b, STEAL ? qx[cc.r & 3] : cc.e, pre_l, pre_r);
         ext_l = __any_sync(FULL, pre_l != NEG) ? warp_max(pre_l) : NEG;
         ext_r = __any_sync(FULL, pre_r != NEG) ? warp_max(pre_r) : NEG;
       }
@@ -1302,6 +1566,9 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
     }
 
     // right anchor: the unit's next blocks inside the window, then EXT
+    if constexpr (STEAL) {
+      if (cc.b + 1 >= cc.e) cc.e = qe[cc.r & 3];  // at the known end: has the owner claimed more?
+    }
     const int nrem = cc.e - cc.b - 1;
     S right = ext_r;
 #pragma unroll
@@ -1447,6 +1714,43 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
       HOOD_CHECK(!hs.in_smem || hs.n <= HC);
       if (hs.in_smem && !written)
         for (long long e = lane; e < hs.n; e += 32) gout[ubase + e] = Hs[e];
+      bool publish = true;
+      long long uend_blk = cc.b + 1;  // the unit's end block (the part's for unstolen units)
+      if constexpr (STEAL) {
+        const int j = cc.r & 3;
+        const int fl = qf[j];
+        uend_blk = qx[j];
+        if (fl) {
+          // a unit in two parts: this part's hood is published for the
+          // other; the later of the two merges them and publishes the unit
+          const int part = fl & 1;
+          if (lane == 0) {
+            p.part_cnt[2 * u + part] = (int)hs.n;
+            p.part_base[2 * u + part] = ubase;
+          }
+          __syncwarp();
+          int prev = 0;
+          if (lane == 0) {
+            __threadfence();  // this part's hood and record before the count
+            prev = atomicAdd(p.steal_done + u, 1);
+            __threadfence();  // ... and the other part's after it
+          }
+          prev = __shfl_sync(FULL, prev, 0);
+          if (prev == 0) {
+            publish = false;
+          } else {
+            const int oc = __ldcg(p.part_cnt + 2 * u + (part ^ 1));
+            const long long ob = __ldcg(p.part_base + 2 * u + (part ^ 1));
+            const Merged mg = part ? merge_parts<V>(gout, ob, oc, ubase, hs.n) : merge_parts<V>(gout, ubase, hs.n, ob, oc);
+            hs.n = mg.n;
+            hs.in_smem = 0;
+            ubase = mg.base;
+            if (lane == 0) p.steal_done[u] = 0;  // for the next build
+            __syncwarp();
+          }
+        }
+      }
+      if (publish) {
       if (spi > 1) {
         // anchor point for finalize: the unit's highest hood corner (a real
         // input point; y along a hood is unimodal, so a spilled hood is searched)
@@ -1492,7 +1796,7 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
           // before it also full, the seam's two monotone-chain triples are
           // input triples -- checked here, so a finalize that sees every unit
           // counted has nothing left to merge
-          const long long uend = min(n, (long long)(cc.b + 1) * BP);
+          const long long uend = min(n, uend_blk * BP);
           if (hs.n == uend - ubase) {
             bool ok = true;
             if (ubase >= 1) {
@@ -1508,9 +1812,11 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
         __threadfence();  // cumulative: covers the lanes' writes ordered by the __syncwarp
         atomicAdd(p.arrive, 1u);
       }
+      }  // publish
       fresh = true;
     }
-    advance(cc);
+    if constexpr (STEAL) sadv(cc);
+    else advance(cc);
   }
   cp_async_wait<0>();
   if (kTrace && p.trace && lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(p.trace) + 1, gtimer());
@@ -1909,10 +2215,15 @@ __device__ __noinline__ void finalize_body(const FinalizeParams<S> p) {
     // this skips the wait for the ring grid's completion
     if (tid == 0) {
       unsigned v;
+      const unsigned long long t0 = gtimer();
       for (;;) {
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.arrive) : "memory");
         if (v >= p.arrive_target) break;
         __nanosleep(32);
+        if (gtimer() - t0 > 4000000000ull) {  // 4 s: a unit never published -- fail, do not hang
+          printf("hood_b200: finalize waited 4 s for %u of %u units\n", v, p.arrive_target);
+          __trap();
+        }
       }
     }
     __syncthreads();
@@ -2665,6 +2976,7 @@ static const DevLaunchState& dev_state() {
     st.inst_occ = occ_of(instance_hull_kernel<S>, inst_smem_bytes<S>(), kThreads);
     occ_of(ring_hull_kernel<S, kRingD, kRingP, kRingU, true, true>, ring_smem<S, true>(), 32 * kRingWarps);
     occ_of(ring_hull_kernel<S, kRingD, kRingP, kRingU, false, true>, ring_smem<S, false>(), 32 * kRingWarps);
+    occ_of(ring_hull_kernel<S, kRingD, kRingP, kRingU, false, false, true>, ring_smem<S, false>(), 32 * kRingWarps);
     cudaFuncSetAttribute(finalize_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     st.fin_attr = true;
     st.ring_occ = occ_of(ring_hull_kernel<S, kRingD, kRingP, kRingU, false>, ring_smem<S, false>(),
@@ -2724,6 +3036,8 @@ void launch_slab_kernel(const SlabParams<S>& p, const CUtensorMap* tmap, int gri
   if (p.check_triples) {
     if (p.lean) cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kRingU, true, true>, p);
     else cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kRingU, false, true>, p);
+  } else if (p.steal_w && !p.lean) {
+    cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kRingU, false, false, true>, p);
   } else {
     if (p.lean) cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kRingU, true, false>, p);
     else cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kRingU, false, false>, p);

@@ -58,7 +58,7 @@ struct SlabParams {
   DevError* err;
   int check_range;          // also flag x outside (0,1) (validate_points)
   int check_triples;        // also flag consecutive triples within the collinearity margin
-  int dbg;                  // 0 normal; 1 stream only (profiling); 2 no merger work
+  int dbg;                  // tests only: 4 = odd warps start 300 us late (forces steals)
   long long* trace;         // optional per-tile clock64 trace (profiling)
   long long read_lim;       // points at or past this index may not be read yet (host-path chunks)
   int lean;                 // ring kernel: the register-light variant (batched builds)
@@ -67,6 +67,16 @@ struct SlabParams {
   // whose left seam continues the unit before it concavely (arc-like input);
   // when every unit counts, the finalize's answer is the input itself
   unsigned* full_units;
+  // tail stealing (multi-unit instances, the STEAL kernel): per unit a claim
+  // word (low 32 bits: blocks the owner has claimed from the front; high 32:
+  // blocks stolen from the end, 0 = none), a parts-done counter, and per part
+  // (2u owner, 2u+1 stolen tail) its hood's corner count and base slot
+  unsigned long long* steal_w;  // [63:48] build epoch, [47:32] stolen blocks, [31:0] claimed blocks
+  unsigned steal_epoch;         // this build's epoch (a word of another build is never stolen from)
+  unsigned* steal_count;        // +1 per steal (tests / diagnosis)
+  int* steal_done;
+  int* part_cnt;
+  long long* part_base;
 };
 
 template <class S>

@@ -1010,3 +1010,60 @@ def test_reference_unit_tests_through_dropin(name):
     observer) against the drop-in, with a minimal doctest stand-in."""
     rc, out = _run_bin(name)
     assert rc == 0 and "0 failed" in out, out
+
+
+# ------------------------------------------------------------- tail stealing
+
+def _steal_lib():
+    import ctypes
+    L = H.library()
+    L.hood_internal_set_debug.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+    L.hood_internal_steals.restype = ctypes.c_longlong
+    L.hood_internal_steals.argtypes = [ctypes.c_void_p]
+    return L
+
+
+@pytest.mark.parametrize("shape", ["gauss26", "arc25", "dent25", "multi"])
+def test_tail_stealing_parity(oracle_mod, shape):
+    """Work stealing of unit tails (the STEAL ring kernel): with every odd
+    warp held back 300 us (debug mode 4) the others steal the back halves of
+    those units, the two parts of each stolen unit are merged by bridge +
+    splice, and the hood is still the oracle's, bit for bit -- single builds,
+    multi-instance builds and the chunked host path."""
+    L = _steal_lib()
+    ctx = H.Context.get(0)
+    rng = np.random.default_rng(7)
+    block = 0
+    if shape == "gauss26":
+        p = W.gauss(1 << 26, seed=62)
+    elif shape == "arc25":
+        p = W.arc(1 << 25)
+    elif shape == "dent25":  # an arc with random dents: survivors everywhere, merge trees, bridges
+        p = W.arc(1 << 25)
+        k = rng.choice(p.shape[0], size=1 << 16, replace=False)
+        p[k, 1] -= rng.random(k.size) * 1e-3
+    else:
+        p = np.concatenate([W.gauss(1 << 24, seed=63 + i) for i in range(4)])
+        block = 1 << 24
+    t = torch.as_tensor(p).cuda()
+    L.hood_internal_steals(ctx.handle)
+    L.hood_internal_set_debug(ctx.handle, 4, None)
+    try:
+        rep = H.build_hood(t, block_len=block)
+        steals = L.hood_internal_steals(ctx.handle)
+        if block:
+            c, corners = rep.counts.cpu().numpy(), rep.corners.cpu().numpy()
+            for i in range(p.shape[0] // block):
+                assert same(corners[i * block: i * block + c[i]], oracle_mod.upper_hull(p[i * block:(i + 1) * block])), i
+        else:
+            got = rep.hull.cpu().numpy()
+            assert same(got, oracle_mod.upper_hull(p)), shape
+            if shape == "gauss26":  # the chunked host path with steals
+                out, cnt = H.build_hood_host(np.ascontiguousarray(p))
+                assert same(out[: cnt[0]], got)
+    finally:
+        L.hood_internal_set_debug(ctx.handle, 0, None)
+    assert steals > 0, shape
+    # and the normal mode after it: the claim words of the slowed build
+    # never leak into the next one
+    assert same(H.build_hood(t, block_len=block).counts.cpu().numpy(), rep.counts.cpu().numpy())
