@@ -1102,7 +1102,7 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
   int* qf = qu + LY::QN;                         // [QN] 1: a stolen tail, 2: an owner range stolen from
   int* qx = qf + LY::QN;                         // [QN] the unit's end block (edge anchors)
 #ifndef HOOD_STEAL_G
-#define HOOD_STEAL_G 8
+#define HOOD_STEAL_G 16
 #endif
 #ifndef HOOD_STEAL_MIN
 #define HOOD_STEAL_MIN 8
