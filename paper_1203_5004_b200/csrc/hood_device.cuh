@@ -212,6 +212,71 @@ __device__ __noinline__ void bridge(const AccA& A, i64 as, i64 m, const AccB& B,
   qidx = tangent_from(A.ld(as + lo), B, bs, k);
 }
 
+// The same bridge by a whole warp (every lane calls it; the result is on
+// every lane): the north star's warp-level common-tangent search.  Both
+// monotone searches go 32-ary -- each round the lanes evaluate the predicate
+// at 32 points spread over the open interval and one ballot keeps the gap
+// between the last true and the first false probe -- so a search over m
+// corners takes ceil(log32 m) rounds instead of log2 m dependent steps.  For
+// LOW_f each lane runs its own tangent search into Q.  Same predicates, same
+// answer as bridge() on every input whose predicates are monotone (every
+// input off rounding-level degeneracy).
+template <class V, class AccB>
+__device__ i64 tangent_from_warp(const V& p, const AccB& B, i64 bs, i64 k) {
+  const int lane = threadIdx.x & 31;
+  // first j in [0, k-1] with !LOW(p, j), LOW(j) = !above(p, q_j, q_{j+1}); LOW(k-1) is false
+  i64 lo = 0, hi = k - 1;
+  while (lo < hi) {
+    const i64 span = hi - lo;  // probes lo + span*l/32 for l < 32, all < hi
+    const i64 j = lo + span * lane / 32;
+    const bool low = j < hi && !above(p, B.ld(bs + j), B.ld(bs + j + 1));
+    const unsigned tm = __ballot_sync(0xffffffffu, low);
+    // LOW is monotone: probes 0 .. c-1 true, c .. false (c = the count of trues)
+    const int c = __popc(tm);
+    const i64 nlo = c == 0 ? lo : lo + span * (c - 1) / 32 + 1;
+    const i64 nhi = c == 32 ? hi : lo + span * c / 32;
+    lo = nlo;
+    hi = max(nhi, nlo);  // (a non-monotone ballot, rounding-level degenerate input: still terminates)
+  }
+  return lo;
+}
+
+template <class V, class AccA, class AccB>
+__device__ __noinline__ void bridge_warp(const AccA& A, i64 as, i64 m, const AccB& B, i64 bs, i64 k, i64& pidx,
+                                         i64& qidx) {
+  const int lane = threadIdx.x & 31;
+  {  // the concatenation test (the pinpoint phase at (m-1, 0), kernel.cpp:101-112)
+    const V pl = A.ld(as + m - 1);
+    const V q0 = B.ld(bs);
+    const bool g_eq = (k == 1) || above(pl, q0, B.ld(bs + 1));
+    const bool f_eq = (m == 1) || above(A.ld(as + m - 2), pl, q0);
+    if (g_eq && f_eq) {
+      pidx = m - 1;
+      qidx = 0;
+      return;
+    }
+  }
+  // first i in [0, m-1] with !LOW_f(i); LOW_f(m-1) is false
+  i64 lo = 0, hi = m - 1;
+  while (lo < hi) {
+    const i64 span = hi - lo;
+    const i64 i = lo + span * lane / 32;
+    bool low = false;
+    if (i < hi) {
+      const V pi = A.ld(as + i);
+      low = above(pi, A.ld(as + i + 1), B.ld(bs + tangent_from(pi, B, bs, k)));
+    }
+    const unsigned tm = __ballot_sync(0xffffffffu, low);
+    const int c = __popc(tm);
+    const i64 nlo = c == 0 ? lo : lo + span * (c - 1) / 32 + 1;
+    const i64 nhi = c == 32 ? hi : lo + span * c / 32;
+    lo = nlo;
+    hi = max(nhi, nlo);
+  }
+  pidx = lo;
+  qidx = tangent_from_warp(A.ld(as + lo), B, bs, k);
+}
+
 // Merge node Q = (bs, k) into node P = (as, m) living in the same storage:
 // result P[..pidx] ++ Q[qidx..] stays at `as` (Q's tail slides left, the
 // reference's splice, kernel.cpp:117-137, without padding).  One thread.

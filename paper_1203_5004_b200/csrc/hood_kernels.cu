@@ -501,12 +501,10 @@ __device__ __noinline__ HoodState merge_block_tree(typename PointT<S>::V* SB, in
   warp_tree_merge<V>(PtrAcc<V>{SB}, mns, mnc, 32, 5, lane);
   const long long qs = mns[0], kq = mnc[0];
   long long pidx = -1, qidx = 0;
-  if (lane == 0 && h.n > 0) {
-    if (h.in_smem) bridge<V>(PtrAcc<V>{Hs}, 0, h.n, PtrAcc<V>{SB}, qs, kq, pidx, qidx);
-    else bridge<V>(PtrAcc<V>{gslab}, 0, h.n, PtrAcc<V>{SB}, qs, kq, pidx, qidx);
+  if (h.n > 0) {  // the warp-parallel common-tangent search (every lane gets the result)
+    if (h.in_smem) bridge_warp<V>(PtrAcc<V>{Hs}, 0, h.n, PtrAcc<V>{SB}, qs, kq, pidx, qidx);
+    else bridge_warp<V>(PtrAcc<V>{gslab}, 0, h.n, PtrAcc<V>{SB}, qs, kq, pidx, qidx);
   }
-  pidx = __shfl_sync(0xffffffffu, pidx, 0);
-  qidx = __shfl_sync(0xffffffffu, qidx, 0);
   const long long newN = pidx + 1 + kq - qidx;
   if (h.in_smem && newN > HC) {  // spill the kept prefix to the output slots
     for (long long i = lane; i <= pidx; i += 32) gslab[i] = Hs[i];
@@ -875,6 +873,26 @@ struct CgAcc {
   __device__ __forceinline__ void st(long long i, V v) const { p[i] = v; }
 };
 
+// The finalize's merge tree reads a node's hood through its leaves' ranges:
+// virtual position g lives in leaf s (the largest with pre[s] <= g), at
+// lb[s] + (g - pre[s]) in HBM.
+template <class V>
+struct VirtAcc {
+  const V* g;
+  const long long* lb;
+  const int* pre;
+  int M;
+  __device__ __forceinline__ V ld(long long gpos) const {
+    int lo = 0, hi = M;
+    while (lo < hi - 1) {
+      const int mid = (lo + hi) >> 1;
+      if (pre[mid] <= gpos) lo = mid;
+      else hi = mid;
+    }
+    return g[lb[lo] + (gpos - pre[lo])];
+  }
+};
+
 struct Merged {
   long long n, base;
 };
@@ -891,9 +909,7 @@ __device__ __noinline__ Merged merge_parts(V* g, long long bP, long long cP, lon
   if (cQ == 0) return Merged{cP, bP};
   if (cP == 0) return Merged{cQ, bQ};
   long long pidx = 0, qidx = 0;
-  if (lane == 0) bridge<V>(CgAcc<V>{g}, bP, cP, CgAcc<V>{g}, bQ, cQ, pidx, qidx);
-  pidx = __shfl_sync(0xffffffffu, pidx, 0);
-  qidx = __shfl_sync(0xffffffffu, qidx, 0);
+  bridge_warp<V>(CgAcc<V>{g}, bP, cP, CgAcc<V>{g}, bQ, cQ, pidx, qidx);
   const long long len = cQ - qidx, dst = bP + pidx + 1, src = bQ + qidx;
   if (dst != src) {
     for (long long e0 = 0; e0 < len; e0 += 32) {
@@ -2562,29 +2578,111 @@ __device__ __noinline__ void finalize_body(const FinalizeParams<S> p) {
         }
       }
       inplace = __syncthreads_and(inplace);
-      if (!inplace) ok = 0;  // general compaction: leave it to the merge tree
+      if (!inplace) ok = 2;  // convex seams, runs not in place: compaction only
     }
   }
-  if (ok) {
+  if (ok == 1) {
     if (tid == 0) p.out_counts[blockIdx.x] = tot;
     if (kTrace && p.trace && tid == 0) p.trace[21] = clock64();
     return;
   }
-  int levels = 0;
-  while ((1 << levels) < M) ++levels;
-  tree_merge<V>(PtrAcc<V>{gout}, nsd, ncd, M, levels);
-  if (kTrace && p.trace && tid == 0) p.trace[21] = clock64();
-  // the merged hood to the instance's first slots: a forward copy in chunks
-  // (every chunk is read before it is written, destination below source)
-  const long long st = nsd[0];
-  const int hc = ncd[0];
-  __syncthreads();
-  if (st != ibase) {
-    for (int c0 = 0; c0 < hc; c0 += kFinThreads) {
-      const int e = c0 + tid;
-      const V v = e < hc ? gout[st + e] : NOPT;
+  // Merge tree WITHOUT data movement.  Leaf s keeps the range
+  // [nsd[s], nsd[s] + ncd[s]) of its slab's hood; a merge only trims the left
+  // node's tail and the right node's head (the splice, kernel.cpp:117-137), so
+  // a node's hood is always its leaves' ranges in order, addressed through the
+  // prefix sums pre[] of their lengths (VirtAcc).  Each pair's common tangent
+  // is found by a warp (bridge_warp); the data moves once, at the end.
+  int* pre = reinterpret_cast<int*>(smem_raw + o_stg);  // [M + 1] (the staging area is free here)
+  auto prefix = [&]() {
+    int mine = 0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int s = tid * per + j;
+      if (j < per && s < M) mine += ncd[s];
+    }
+    int tot2 = 0;
+    int off = block_excl_sum<NWP>(mine, shI, &tot2);
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int s = tid * per + j;
+      if (j < per && s < M) {
+        pre[s] = off;
+        off += ncd[s];
+      }
+    }
+    if (tid == 0) pre[M] = tot2;
+    __syncthreads();
+  };
+  auto leaf_of = [&](long long gpos, int lo, int hi) {  // the largest s in [lo, hi) with pre[s] <= gpos
+    while (lo < hi - 1) {
+      const int mid = (lo + hi) >> 1;
+      if (pre[mid] <= gpos) lo = mid;
+      else hi = mid;
+    }
+    return lo;
+  };
+  if (ok == 0) {
+    int levels = 0;
+    while ((1 << levels) < M) ++levels;
+    for (int l = 0; l < levels; ++l) {
+      prefix();
+      const int half = 1 << l, span = half << 1;
+      for (int a = warp * span; a < M; a += NWP * span) {
+        const int b = a + half;
+        if (b >= M) continue;
+        const int e = min(a + span, M);
+        const int m = pre[b] - pre[a], k = pre[e] - pre[b];
+        if (m == 0 || k == 0) continue;
+        const VirtAcc<V> X{gout, nsd, pre, M};
+        long long pidx = 0, qidx = 0;
+        bridge_warp<V>(X, (long long)pre[a], (long long)m, X, (long long)pre[b], (long long)k, pidx, qidx);
+        if (lane == 0) {
+          const long long gp = pre[a] + pidx;  // P keeps [0, pidx]
+          const int sp = leaf_of(gp, a, b);
+          ncd[sp] = (int)(gp - pre[sp]) + 1;
+          for (int t = sp + 1; t < b; ++t) ncd[t] = 0;
+          const long long gq = pre[b] + qidx;  // Q keeps [qidx, k)
+          const int sq = leaf_of(gq, b, e);
+          const int off = (int)(gq - pre[sq]);
+          nsd[sq] += off;
+          ncd[sq] -= off;
+          for (int t = b; t < sq; ++t) ncd[t] = 0;
+        }
+        __syncwarp();
+      }
       __syncthreads();
-      if (e < hc) gout[ibase + e] = v;
+    }
+  }
+  prefix();
+  const int hc = pre[M];
+  if (kTrace && p.trace && tid == 0) p.trace[21] = clock64();
+  // the leaves' ranges to the instance's first slots: a forward copy in chunks
+  // (every chunk is read before any of it is written; every destination is at
+  // or left of its source)
+  int moved = 0;
+  for (int s0 = tid; s0 < M; s0 += kFinThreads) moved |= ncd[s0] > 0 && nsd[s0] != ibase + pre[s0];
+  if (__syncthreads_or(moved)) {
+    constexpr int EPT = 8;  // elements per thread per chunk, loads in flight together
+    for (long long c0 = 0; c0 < hc; c0 += (long long)kFinThreads * EPT) {
+      const long long e0 = c0 + (long long)tid * EPT;
+      V v[EPT];
+      if (e0 < hc) {
+        int sl = leaf_of(e0, 0, M);
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) {
+          const long long e = e0 + i;
+          if (e < hc) {
+            while (e >= pre[sl + 1]) ++sl;
+            v[i] = gout[nsd[sl] + (e - pre[sl])];
+          }
+        }
+      }
+      __syncthreads();
+      if (e0 < hc) {
+#pragma unroll
+        for (int i = 0; i < EPT; ++i)
+          if (e0 + i < hc) gout[ibase + e0 + i] = v[i];
+      }
       __syncthreads();
     }
   }
