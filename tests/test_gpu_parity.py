@@ -1067,3 +1067,24 @@ def test_tail_stealing_parity(oracle_mod, shape):
     # and the normal mode after it: the claim words of the slowed build
     # never leak into the next one
     assert same(H.build_hood(t, block_len=block).counts.cpu().numpy(), rep.counts.cpu().numpy())
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_dented_and_noisy_arcs(oracle_mod, dtype):
+    """Arc-like inputs with imperfections: every block has many survivors but
+    not a concave chain (the warp merge tree + bridge_warp), unit hoods of
+    thousands of corners with non-convex seams (the finalize's range-based
+    merge tree and its one compaction).  Bit-exact against the oracle."""
+    rng = np.random.default_rng(11)
+    for n, dents, depth in [(1 << 20, 1 << 12, 1e-4), (1 << 20, 1 << 18, 1e-6), (3 << 18, 1 << 10, 1e-2)]:
+        p = W.arc(n)
+        if dtype == torch.float32:
+            p = p.astype(np.float32).astype(np.float64)
+            keep = np.concatenate([[True], np.diff(p[:, 0]) > 0])
+            p = p[keep]
+        k = rng.choice(p.shape[0], size=min(dents, p.shape[0] // 2), replace=False)
+        p[k, 1] -= rng.random(k.size) * depth
+        if dtype == torch.float32:
+            p = p.astype(np.float32)
+        want = oracle_mod.upper_hull(p.astype(np.float64))
+        assert same(gpu_hull(p, dtype=dtype).astype(np.float64), want), (n, dents, depth)
