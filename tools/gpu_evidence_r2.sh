@@ -15,5 +15,9 @@ for c in 2 3 4 5; do
 done
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"finalize" --launch-skip 3 -c 1 -o gpurun_out/ev/prof_fin_c2 -f python bench.py --config 2 --steps 1 --warmup 3 --no-e2e --no-kernel-events --cpu-seconds 0.01 > gpurun_out/ev/ncu_fin_c2.log 2>&1
 export HOOD_B200_LIB=$PWD/paper_1203_5004_b200/lib/libhood_b200_trace.so
-timeout 300 python tools/trace_ring.py 24 g26 a22 b > gpurun_out/ev/trace_ring.log 2>&1
+NOEV=1 timeout 600 python tools/trace_ring.py 24 g28 a22 b > gpurun_out/ev/trace_ring.log 2>&1
 timeout 300 python tools/trace_finalize.py 2 > gpurun_out/ev/trace_fin_c2.log 2>&1
+unset HOOD_B200_LIB
+for c in 3 4; do timeout 600 ncu --metrics smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_executed_op_ffma_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,gpu__time_duration.sum -k regex:"ring_hull|finalize" --launch-skip 6 -c 2 python bench.py --config $c --steps 1 --warmup 3 --no-e2e --no-kernel-events --cpu-seconds 0.01 > gpurun_out/ev/ncu_dfma_c$c.log 2>&1; done
+python tools/steal_diag.py > gpurun_out/ev/steal_diag.log 2>&1
+python tools/time_dent.py > gpurun_out/ev/time_dent.log 2>&1
