@@ -138,6 +138,12 @@ int make_plan(hood_ctx* ctx, long long n, long long block_len, Plan& pl) {
     // batched builds (every unit a whole instance, more instances than warps)
     // run the register-light ring variant at higher occupancy
     pl.lean = pl.spi == 1 && pl.instances > 1 && ring_lean_available<S>();
+    if (pl.lean && slab_tile_rows<S>(true, true) != pl.rows) {  // the LEAN variant's own block size
+      pl.rows = slab_tile_rows<S>(true, true);
+      pl.T = (long long)pl.rows * K;
+      pl.tiles = (n + pl.T - 1) / pl.T;
+      pl.tpi = (pl.L + pl.T - 1) / pl.T;
+    }
     const long long ctas_run = pl.lean ? (long long)slab_kernel_occupancy<S>(true) * ctx->sms : ctas;
     pl.grid = (int)std::min((pl.units + nw - 1) / nw, ctas_run);
   } else {
@@ -178,14 +184,16 @@ int ensure_ws(hood_ctx* ctx, long long slabs) {
         cudaMalloc(&ctx->seg_base, cap * sizeof(long long)) != cudaSuccess ||
         cudaMalloc(&ctx->steal_w, cap * sizeof(unsigned long long)) != cudaSuccess ||
         cudaMalloc(&ctx->steal_done, cap * sizeof(int)) != cudaSuccess ||
-        cudaMalloc(&ctx->part_cnt, 2 * cap * sizeof(int)) != cudaSuccess ||
-        cudaMalloc(&ctx->part_base, 2 * cap * sizeof(long long)) != cudaSuccess)
+        cudaMalloc(&ctx->part_cnt, kStealParts * cap * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&ctx->part_base, kStealParts * cap * sizeof(long long)) != cudaSuccess)
       return HOOD_ERR_CUDA;
     // claim words start "not stealable" (a stolen count != 0); every owner
     // resets its own word at the start of each build, and every build leaves
-    // every word in a state no thief takes (fully claimed, or stolen once)
+    // every word in a state no thief takes (fully claimed); part counts
+    // start (and are left by every merge) at -1 = no such part
     if (cudaMemset(ctx->steal_w, 0xff, cap * sizeof(unsigned long long)) != cudaSuccess ||
-        cudaMemset(ctx->steal_done, 0, cap * sizeof(int)) != cudaSuccess)
+        cudaMemset(ctx->steal_done, 0, cap * sizeof(int)) != cudaSuccess ||
+        cudaMemset(ctx->part_cnt, 0xff, kStealParts * cap * sizeof(int)) != cudaSuccess)
       return HOOD_ERR_CUDA;
     ctx->seg_cap = cap;
   }

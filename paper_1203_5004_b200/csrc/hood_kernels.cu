@@ -560,6 +560,12 @@ __device__ __forceinline__ void cp_async_wait() {
 #ifndef HOOD_LEAN_HC
 #define HOOD_LEAN_HC 128
 #endif
+#ifndef HOOD_LEAN_U
+#define HOOD_LEAN_U 8
+#endif
+#ifndef HOOD_LEAN_NREG
+#define HOOD_LEAN_NREG 128
+#endif
 #ifndef HOOD_HC
 #define HOOD_HC 128
 #endif
@@ -1038,7 +1044,7 @@ __device__ __noinline__ AppendRes append_full_block(unsigned a, unsigned slot_ba
 // stolen unit are merged by the later of them (bridge + splice) into the
 // unit's one segment, so the finalize is unchanged.
 template <class S, int D, int P, int U_, bool LEAN = false, bool TRI = false, bool STEAL = false>
-__global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams<S> p) {
+__global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams<S> p) {
   using V = typename PointT<S>::V;
   using L = typename Ld16<S>::T;
   using LY = RingLayout<S, D, P, U_, LEAN>;
@@ -1120,17 +1126,27 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
 #ifndef HOOD_STEAL_G
 #define HOOD_STEAL_G 16
 #endif
+#ifndef HOOD_STEAL_GS
+#define HOOD_STEAL_GS 4
+#endif
+#ifndef HOOD_STEAL_TAIL
+#define HOOD_STEAL_TAIL 64
+#endif
 #ifndef HOOD_STEAL_MIN
-#define HOOD_STEAL_MIN 8
+#define HOOD_STEAL_MIN 4
 #endif
   constexpr int kG = HOOD_STEAL_G;            // blocks per owner claim (the next claim is in flight a whole claim ahead)
+  constexpr int kGs = HOOD_STEAL_GS;          // ... once at most kTail blocks are left unclaimed
+  constexpr int kTail = HOOD_STEAL_TAIL;
   constexpr int kMinSteal = HOOD_STEAL_MIN;   // smallest stolen tail (blocks)
+  constexpr int kMaxSteals = kStealParts - 1; // steals per unit
   int ci_r = 0;                 // range number of the issue cursor
   int ci_mode = 0;              // 0 owner, 1 search, 2 stolen range, 3 done
   int ci_b = 0;                 // next block to issue
   int claimed_to = 0;           // owner: end of its claimed blocks
   // cold state in smem (touched once per claim or range): [0] a claim in
-  // flight, [1] blocks stolen from the owner's unit, [2] the stolen range's end
+  // flight, [1] blocks stolen from the owner's unit, [2] the stolen range's
+  // end, [3] the size of the claim in flight
   int* cs = qx + LY::QN;
   // the owner's unit: qb[0] .. qx[0] (queue slot 0 holds range 0 while the owner claims)
   const long long own_u = p.unit_lo + gw;
@@ -1143,22 +1159,26 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
   // the back half of the unit with the most unclaimed blocks among 32
   // sampled units (all of them when there are at most 32), one CAS; one L2
   // round trip per attempt, attempts repeated only when the CAS loses a race
-  auto steal = [&](int& sb, int& se, int& sv) -> bool {
+  int s_seq = 0;  // samples taken so far
+  auto steal = [&](int& sb, int& se, int& sv, int& sk) -> bool {
     const long long units = p.unit_hi - p.unit_lo;
     for (int attempt = 0; attempt < 4; ++attempt) {
       long long best = 0;
       int bvu = -1;
       unsigned long long bold = 0;
       {
-        const unsigned h = ((unsigned)gw * 131u + (unsigned)attempt * 977u + (unsigned)lane * 61u) * 2654435761u;
+        // a fresh sample on every attempt of every steal (a thief back for
+        // more must not see the units it has just emptied)
+        const unsigned h = ((unsigned)gw * 131u + (unsigned)(s_seq++) * 977u + (unsigned)lane * 61u) * 2654435761u;
         const long long vv = units <= 32 ? (long long)lane : (long long)((h >> 7) % (unsigned)units);
         const unsigned long long w =
             vv < units ? *reinterpret_cast<volatile unsigned long long*>(p.steal_w + p.unit_lo + vv) : ~0ull;
-        if ((w >> 32) == ((unsigned long long)p.steal_epoch << 16)) {  // this build's, nothing stolen
+        // this build's word, fewer than kMaxSteals steals so far
+        if ((w >> 48) == (unsigned long long)p.steal_epoch && (int)((w >> 44) & 0xf) < kMaxSteals) {
           const long long v = p.unit_lo + vv;
           int b0, b1;
           unit_range(v, b0, b1);
-          const long long rem = (long long)(b1 - b0) - (long long)(unsigned)w;
+          const long long rem = (long long)(b1 - b0) - (long long)((w >> 32) & 0xfff) - (long long)(unsigned)w;
           if (rem > best) {
             best = rem;
             bvu = (int)v;
@@ -1177,18 +1197,20 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
           bold = oo;
         }
       }
-      if (best < 2 * kMinSteal) return false;
-      const int K = (int)min(best / 2, 0xffffLL);
+      const int S0 = (int)((bold >> 32) & 0xfff);
+      const int K = (int)min(best / 2, (long long)(0xfff - S0));
+      if (best < 2 * kMinSteal || K < kMinSteal) return false;
       unsigned long long got = 0;
-      if (lane == 0) got = atomicCAS(p.steal_w + bvu, bold, bold + ((unsigned long long)K << 32));
+      if (lane == 0) got = atomicCAS(p.steal_w + bvu, bold, bold + ((unsigned long long)K << 32) + (1ull << 44));
       got = __shfl_sync(FULL, got, 0);
       if (got == bold) {
         if (lane == 0 && p.steal_count) atomicAdd(p.steal_count, 1u);
         int b0, b1;
         unit_range(bvu, b0, b1);
-        sb = b1 - K;
-        se = b1;
+        sb = b1 - S0 - K;
+        se = b1 - S0;
         sv = bvu;
+        sk = (int)((bold >> 44) & 0xf) + 1;  // its part: steal k takes the blocks left of steal k-1's
         return true;
       }
     }
@@ -1203,18 +1225,23 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
         if (cs[0]) {  // consume the claim in flight
           const unsigned long long pv = __shfl_sync(FULL, own_pend, 0);
           const int f = (int)(unsigned)pv;
-          const int own_s = (int)((pv >> 32) & 0xffffu);
-          const int cnt = max(0, min(kG, (own_b1 - own_s) - (own_b0 + f)));
+          const int own_s = (int)((pv >> 32) & 0xfff);
+          const int own_k = (int)((pv >> 44) & 0xf);
+          const int cnt = max(0, min(cs[3], (own_b1 - own_s) - (own_b0 + f)));
           __syncwarp();
           if (lane == 0) {
             cs[0] = 0;
             cs[1] = own_s;
+            qf[ci_r & 3] = own_k << 2;  // steals so far (final once the range ends)
           }
           if (cnt > 0) {
             claimed_to = own_b0 + f + cnt;
-            if (claimed_to < own_b1 - own_s && lane == 0) {
-              own_pend = atomicAdd(p.steal_w + own_u, (unsigned long long)kG);
+            const int left = own_b1 - own_s - claimed_to;
+            if (left > 0 && lane == 0) {
+              const int g = left > kTail ? kG : kGs;  // small claims near the end: less to steal around
+              own_pend = atomicAdd(p.steal_w + own_u, (unsigned long long)g);
               cs[0] = 1;
+              cs[3] = g;
             }
             if (lane == 0) qe[ci_r & 3] = claimed_to;
             __syncwarp();
@@ -1226,15 +1253,15 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
         ci_mode = 1;
       }
       if (ci_mode == 1) {
-        int sb, se, sv;
-        if (steal(sb, se, sv)) {
+        int sb, se, sv, sk;
+        if (steal(sb, se, sv, sk)) {
           ++ci_r;
           if (lane == 0) {
             const int j = ci_r & 3;
             qb[j] = sb;
             qe[j] = se;
             qu[j] = sv;
-            qf[j] = 1;
+            qf[j] = 1 | (sk << 2);
             qx[j] = se;
             cs[2] = se;
           }
@@ -1389,16 +1416,18 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
     // claim goes out at once
     claimed_to = min(own_b0 + kG, own_b1);
     if (lane == 0) {
-      // this build's epoch, nothing stolen, the first pair claimed
+      // this build's epoch, nothing stolen, the first claim taken
       p.steal_w[own_u] = ((unsigned long long)p.steal_epoch << 48) | (unsigned long long)(claimed_to - own_b0);
-      if (claimed_to < own_b1) own_pend = atomicAdd(p.steal_w + own_u, (unsigned long long)kG);
+      const int left = own_b1 - claimed_to, g = left > kTail ? kG : kGs;
+      if (left > 0) own_pend = atomicAdd(p.steal_w + own_u, (unsigned long long)g);
       qb[0] = own_b0;
       qe[0] = claimed_to;
       qu[0] = (int)own_u;
       qf[0] = 0;
       qx[0] = own_b1;
-      cs[0] = claimed_to < own_b1;
+      cs[0] = left > 0;
       cs[1] = 0;
+      cs[3] = g;
     }
     __syncwarp();
     if ((p.dbg & 4) && (gw & 1)) {  // tests: a slow half of the warps, so the others steal
@@ -1654,14 +1683,16 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
         total = __shfl_sync(FULL, incl, 31);
       }
       bool appended = false;
-      if (!LEAN && total == BP) {
-        // every point survives (arc-like input): straight to the output
-        // slots when the block continues the hood as a concave chain
-        flush();
-        const AppendRes ar = append_full_block<S, U, HC>(a, ring_s + s_cur * BB, Hs, gout + ubase, htail, hs, ht_ok);
-        hs = ar.h;
-        appended = ar.ok;
-        ht_ok = ar.ok;
+      if constexpr (!LEAN) {
+        if (total == BP) {
+          // every point survives (arc-like input): straight to the output
+          // slots when the block continues the hood as a concave chain
+          flush();
+          const AppendRes ar = append_full_block<S, U, HC>(a, ring_s + s_cur * BB, Hs, gout + ubase, htail, hs, ht_ok);
+          hs = ar.h;
+          appended = ar.ok;
+          ht_ok = ar.ok;
+        }
       }
       if (appended) {
       } else {
@@ -1736,32 +1767,46 @@ __global__ void __maxnreg__(LEAN ? 128 : HOOD_RING_MAXNREG) ring_hull_kernel(con
         const int j = cc.r & 3;
         const int fl = qf[j];
         uend_blk = qx[j];
-        if (fl) {
-          // a unit in two parts: this part's hood is published for the
-          // other; the later of the two merges them and publishes the unit
-          const int part = fl & 1;
+        if (fl & 3) {
+          // a unit in parts (the owner's, then steal k's left of steal k-1's):
+          // this part's hood is published for the others; the last to finish
+          // merges them left to right and publishes the unit.  Done count:
+          // +1 per thief, -k by the owner (k = its unit's steals, final once
+          // its range has ended), so it reaches 0 exactly at the last part.
+          const int part = (fl & 1) ? (fl >> 2) : 0;
           if (lane == 0) {
-            p.part_cnt[2 * u + part] = (int)hs.n;
-            p.part_base[2 * u + part] = ubase;
+            p.part_cnt[kStealParts * u + part] = (int)hs.n;
+            p.part_base[kStealParts * u + part] = ubase;
           }
           __syncwarp();
-          int prev = 0;
+          int now = 1;
           if (lane == 0) {
             __threadfence();  // this part's hood and record before the count
-            prev = atomicAdd(p.steal_done + u, 1);
-            __threadfence();  // ... and the other part's after it
+            const int add = (fl & 1) ? 1 : -(fl >> 2);
+            now = atomicAdd(p.steal_done + u, add) + add;
+            __threadfence();  // ... and the other parts' after it
           }
-          prev = __shfl_sync(FULL, prev, 0);
-          if (prev == 0) {
+          now = __shfl_sync(FULL, now, 0);
+          if (now != 0) {
             publish = false;
           } else {
-            const int oc = __ldcg(p.part_cnt + 2 * u + (part ^ 1));
-            const long long ob = __ldcg(p.part_base + 2 * u + (part ^ 1));
-            const Merged mg = part ? merge_parts<V>(gout, ob, oc, ubase, hs.n) : merge_parts<V>(gout, ubase, hs.n, ob, oc);
-            hs.n = mg.n;
+            int k = 0;  // the unit's steals: the highest part index present
+            for (int i = 1; i < kStealParts; ++i)
+              if (i == part || __ldcg(p.part_cnt + kStealParts * u + i) >= 0) k = i;
+            Merged acc{part == 0 ? hs.n : (long long)__ldcg(p.part_cnt + kStealParts * u),
+                       part == 0 ? ubase : __ldcg(p.part_base + kStealParts * u)};
+            for (int i = k; i >= 1; --i) {
+              const long long qc = i == part ? hs.n : (long long)__ldcg(p.part_cnt + kStealParts * u + i);
+              const long long qb_ = i == part ? ubase : __ldcg(p.part_base + kStealParts * u + i);
+              acc = merge_parts<V>(gout, acc.base, acc.n, qb_, qc);
+            }
+            hs.n = acc.n;
             hs.in_smem = 0;
-            ubase = mg.base;
-            if (lane == 0) p.steal_done[u] = 0;  // for the next build
+            ubase = acc.base;
+            if (lane == 0) {  // for the next build
+              p.steal_done[u] = 0;
+              for (int i = 1; i < kStealParts; ++i) p.part_cnt[kStealParts * u + i] = -1;
+            }
             __syncwarp();
           }
         }
@@ -3037,10 +3082,11 @@ void launch_gather_records(const double* recs, long long G, long long cap, doubl
 // of (1,1,8), (1,2,8), (2,2,8), (2,3,4) on B200 for both storages (round 1,
 // tools/gpu_sweep.sh); the other shapes are no longer compiled.
 constexpr int kRingD = 1, kRingP = 1, kRingU = 8;
+constexpr int kLeanU = HOOD_LEAN_U;  // the batched (LEAN) variant's block: 16-byte chunks per lane
 
 template <class S, bool LEAN>
 static size_t ring_smem() {
-  return RingLayout<S, kRingD, kRingP, kRingU, LEAN>::CTA_BYTES(kRingWarps);
+  return RingLayout<S, kRingD, kRingP, LEAN ? kLeanU : kRingU, LEAN>::CTA_BYTES(kRingWarps);
 }
 
 // Per-device launch state: the dynamic shared-memory opt-in
@@ -3069,10 +3115,10 @@ static const DevLaunchState& dev_state() {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem);
       return o > 0 ? o : 1;
     };
-    st.ring_occ_lean = occ_of(ring_hull_kernel<S, kRingD, kRingP, kRingU, true>, ring_smem<S, true>(),
+    st.ring_occ_lean = occ_of(ring_hull_kernel<S, kRingD, kRingP, kLeanU, true>, ring_smem<S, true>(),
                               32 * kRingWarps);
     st.inst_occ = occ_of(instance_hull_kernel<S>, inst_smem_bytes<S>(), kThreads);
-    occ_of(ring_hull_kernel<S, kRingD, kRingP, kRingU, true, true>, ring_smem<S, true>(), 32 * kRingWarps);
+    occ_of(ring_hull_kernel<S, kRingD, kRingP, kLeanU, true, true>, ring_smem<S, true>(), 32 * kRingWarps);
     occ_of(ring_hull_kernel<S, kRingD, kRingP, kRingU, false, true>, ring_smem<S, false>(), 32 * kRingWarps);
     occ_of(ring_hull_kernel<S, kRingD, kRingP, kRingU, false, false, true>, ring_smem<S, false>(), 32 * kRingWarps);
     cudaFuncSetAttribute(finalize_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -3089,9 +3135,9 @@ bool ring_lean_available() {
 }
 
 template <class S>
-int slab_tile_rows(bool hmode) {
+int slab_tile_rows(bool hmode, bool lean) {
   // hmode: points per ring block, in 128-byte chunk rows of K points
-  return hmode ? 32 * kRingU * Ld16<S>::PPL / PointT<S>::K : kThreads;
+  return hmode ? 32 * (lean ? kLeanU : kRingU) * Ld16<S>::PPL / PointT<S>::K : kThreads;
 }
 
 template <class S>
@@ -3132,12 +3178,12 @@ void launch_slab_kernel(const SlabParams<S>& p, const CUtensorMap* tmap, int gri
   cfg.numAttrs = reset_err ? 1 : 0;
   cfg.dynamicSmemBytes = p.lean ? ring_smem<S, true>() : ring_smem<S, false>();
   if (p.check_triples) {
-    if (p.lean) cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kRingU, true, true>, p);
+    if (p.lean) cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kLeanU, true, true>, p);
     else cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kRingU, false, true>, p);
   } else if (p.steal_w && !p.lean) {
     cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kRingU, false, false, true>, p);
   } else {
-    if (p.lean) cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kRingU, true, false>, p);
+    if (p.lean) cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kLeanU, true, false>, p);
     else cudaLaunchKernelEx(&cfg, ring_hull_kernel<S, kRingD, kRingP, kRingU, false, false>, p);
   }
 }
@@ -3209,7 +3255,7 @@ template int instance_kernel_occupancy<float>();
 template int instance_kernel_occupancy<double>();
 template int slab_warps_per_cta<float>();
 template int slab_warps_per_cta<double>();
-template int slab_tile_rows<float>(bool);
-template int slab_tile_rows<double>(bool);
+template int slab_tile_rows<float>(bool, bool);
+template int slab_tile_rows<double>(bool, bool);
 
 }  // namespace hood_b200

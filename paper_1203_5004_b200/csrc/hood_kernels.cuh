@@ -35,6 +35,9 @@ struct DevError {
 };
 constexpr unsigned long long kTripleKey = 1ULL << 62;
 
+// parts of a unit under tail stealing: the owner's and up to 3 stolen tails
+constexpr int kStealParts = 4;
+
 template <class S>
 struct SlabParams {
   const void* pts;          // n points, {x, y} interleaved, 16-byte aligned
@@ -68,10 +71,11 @@ struct SlabParams {
   // when every unit counts, the finalize's answer is the input itself
   unsigned* full_units;
   // tail stealing (multi-unit instances, the STEAL kernel): per unit a claim
-  // word (low 32 bits: blocks the owner has claimed from the front; high 32:
-  // blocks stolen from the end, 0 = none), a parts-done counter, and per part
-  // (2u owner, 2u+1 stolen tail) its hood's corner count and base slot
-  unsigned long long* steal_w;  // [63:48] build epoch, [47:32] stolen blocks, [31:0] claimed blocks
+  // word (blocks the owner has claimed from the front, blocks stolen from the
+  // end, steals so far), a parts-done counter, and per part (kStealParts u:
+  // the owner's, kStealParts u + k: steal k's) its hood's corner count (-1:
+  // no such part) and base slot
+  unsigned long long* steal_w;  // [63:48] build epoch, [47:44] steals, [43:32] stolen blocks, [31:0] claimed blocks
   unsigned steal_epoch;         // this build's epoch (a word of another build is never stolen from)
   unsigned* steal_count;        // +1 per steal (tests / diagnosis)
   int* steal_done;
@@ -147,7 +151,7 @@ int instance_kernel_occupancy();  // instance-kernel CTAs per SM
 template <class S>
 int slab_warps_per_cta();      // units (warps) per slab-kernel CTA
 template <class S>
-int slab_tile_rows(bool hmode);  // chunk rows (= threads) per tile
+int slab_tile_rows(bool hmode, bool lean = false);  // chunk rows (= threads) per tile
 size_t finalize_smem(int fcap_bytes, int slabs);
 
 }  // namespace hood_b200
