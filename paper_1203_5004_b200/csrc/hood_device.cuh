@@ -354,6 +354,14 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// Running maximum / minimum of y values: acc is never NaN, v may be (a NaN v
+// never replaces acc, as with fmax).  For double a compare and two selects;
+// fmax/fmin add NaN quieting (DSETP.MAX + 3 selects) on the landing pass.
+template <class S> __device__ __forceinline__ S ymax(S acc, S v) { return v > acc ? v : acc; }
+template <> __device__ __forceinline__ float ymax<float>(float acc, float v) { return fmaxf(acc, v); }
+template <class S> __device__ __forceinline__ S ymin(S a, S b) { return b < a ? b : a; }
+template <> __device__ __forceinline__ float ymin<float>(float a, float b) { return fminf(a, b); }
+
 template <class S> __device__ __forceinline__ S neg_inf();
 template <> __device__ __forceinline__ float neg_inf<float>() { return -__int_as_float(0x7f800000); }
 template <> __device__ __forceinline__ double neg_inf<double>() {

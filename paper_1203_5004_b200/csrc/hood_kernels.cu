@@ -903,8 +903,8 @@ struct Merged {
   long long n, base;
 };
 
-// STEAL: the two parts of a stolen unit -- P (the owner's, left) at bP and Q
-// (the thief's tail) at bQ, each a strict upper hood in its output slots --
+// STEAL: two adjacent parts of a stolen unit -- P (left) at bP and Q (the
+// part right of it) at bQ, each a strict upper hood in its output slots --
 // merged into one: the common tangent by bridge() (the g/f classifiers as
 // monotone searches, kernel.hpp:31-67), then the splice P[..pidx] ++ Q[qidx..]
 // (kernel.cpp:117-137) in place at bP (a forward copy: the destination is
@@ -1038,11 +1038,12 @@ __device__ __noinline__ AppendRes append_full_block(unsigned a, unsigned slot_ba
 // on a slot mbarrier -- was measured against this cp.async ring in round 2 and
 // lost on every large config: profiles/r02/ab_tma.md.)
 // STEAL: multi-unit instances balance their tails: each warp claims its
-// unit's blocks from the front in pairs (one claim in flight), and a warp whose
-// work is done steals the back half of the unit with the most unclaimed blocks
-// (one CAS on the unit's claim word; one steal per unit).  The two parts of a
-// stolen unit are merged by the later of them (bridge + splice) into the
-// unit's one segment, so the finalize is unchanged.
+// unit's blocks from the front (16 at a time, 4 near the end; one claim in
+// flight), and a warp whose work is done steals the back half of the unit
+// with the most unclaimed blocks among 32 sampled (one CAS on the unit's
+// claim word; up to kStealParts - 1 steals per unit).  The parts of a stolen
+// unit are merged left to right by the last of them to finish (bridge +
+// splice) into the unit's one segment, so the finalize is unchanged.
 template <class S, int D, int P, int U_, bool LEAN = false, bool TRI = false, bool STEAL = false>
 __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull_kernel(const SlabParams<S> p) {
   using V = typename PointT<S>::V;
@@ -1353,8 +1354,8 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
           const V q = pt_of(c[k], e);
           ok = ok && (q.x > prev);
           prev = q.x;
-          if ((k * PPL + e) & 1) m1 = fmax(m1, q.y);
-          else m0 = fmax(m0, q.y);
+          if ((k * PPL + e) & 1) m1 = ymax<S>(m1, q.y);
+          else m0 = ymax<S>(m0, q.y);
         }
     } else {
       const long long q0 = (long long)b * BP + lane * NP;
@@ -1366,7 +1367,7 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
           const bool valid = q0 + k * PPL + e < n;
           ok = ok && (!valid || q.x > prev);
           prev = q.x;
-          if (valid) m0 = fmax(m0, q.y);
+          if (valid) m0 = ymax<S>(m0, q.y);
         }
     }
     if (p.check_range) {
@@ -1387,7 +1388,7 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
     }
     xc = __shfl_sync(FULL, xl, 31);
     if (__any_sync(FULL, !ok)) report(b, false);
-    return fmax(m0, m1);
+    return ymax<S>(m0, m1);
   };
 
   // a dependent finalize may be scheduled now; it waits for our completion
@@ -1618,8 +1619,8 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
     S right = ext_r;
 #pragma unroll
     for (int i = 0; i < D; ++i)
-      if (i < nrem) right = fmax(right, win[i]);
-    const S tau = fmin(runmax, right);
+      if (i < nrem) right = ymax<S>(right, win[i]);
+    const S tau = ymin<S>(runmax, right);
     const long long bs = (long long)cc.b * BP;
 
     // lane runs reaching tau (every run at an instance edge)
@@ -1731,7 +1732,7 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
     }
     HOOD_TOC(c_cand);
     if (pend > PC - 2 * NP) flush();  // keeps room for two candidate runs
-    runmax = fmax(runmax, wcur);
+    runmax = ymax<S>(runmax, wcur);
     // slide the window: the block after this one becomes current
     lmc = lmw[0];
     wcur = win[0];
