@@ -973,7 +973,7 @@ __device__ __noinline__ AppendRes append_full_block(unsigned a, unsigned slot_ba
     const V& l = i > 0 ? v[i - 1] : prev;
     const V& r = i + 1 < NP ? v[i + 1] : next;
     const bool skip = (i == 0 && lane == 0) || (i == NP - 1 && lane == 31);
-    if (!skip) conc = conc && above(l, v[i], r);
+    if (!skip) conc = conc & above(l, v[i], r);  // no short circuit: independent tests, no branch chain
   }
   if (!__all_sync(FULL, conc)) return AppendRes{h, false};
   bool join = true;
