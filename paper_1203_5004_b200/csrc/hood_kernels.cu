@@ -990,12 +990,19 @@ __device__ __noinline__ AppendRes append_full_block(unsigned a, unsigned slot_ba
     h.in_smem = 0;
   }
   V* dst = gslab + h.n;  // global: plain STG, no generic-address resolution
+  // store k reads corner q = 32k + lane of the slot: row r = q / NP, the
+  // swizzle repeats every 8 rows (ring_rot), i.e. every PER stores, so PER
+  // addresses are computed and the rest are constant offsets from them
+  constexpr int PER = NP / 4 > 0 ? NP / 4 : 1;
+  static_assert(PER * (32 / NP) == 8 || NP < 4, "swizzle period");
+  unsigned adb[PER];
 #pragma unroll
-  for (int k = 0; k < NP; ++k) {
-    const int q = 32 * k + lane, r = q / NP, e = q % NP;
-    const unsigned ad = (slot_base + r * (16 * U) + (((e / PPL) ^ ring_rot<U>(r)) << 4)) + (e % PPL) * (unsigned)sizeof(V);
-    dst[q] = lds_pt(ad, (V*)nullptr);
+  for (int j = 0; j < PER; ++j) {
+    const int q = 32 * j + lane, r = q / NP, e = q % NP;
+    adb[j] = (slot_base + r * (16 * U) + (((e / PPL) ^ ring_rot<U>(r)) << 4)) + (e % PPL) * (unsigned)sizeof(V);
   }
+#pragma unroll
+  for (int k = 0; k < NP; ++k) dst[32 * k + lane] = lds_pt(adb[k % PER] + (unsigned)((k / PER) * 8 * 16 * U), (V*)nullptr);
   if (lane == 31) {
     ht[0] = v[NP - 2];
     ht[1] = v[NP - 1];
