@@ -1143,6 +1143,9 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
 #ifndef HOOD_STEAL_MIN
 #define HOOD_STEAL_MIN 4
 #endif
+#ifndef HOOD_STEAL_PF
+#define HOOD_STEAL_PF 1  // L2 prefetch distance in blocks (0: none)
+#endif
   constexpr int kG = HOOD_STEAL_G;            // blocks per owner claim (the next claim is in flight a whole claim ahead)
   constexpr int kGs = HOOD_STEAL_GS;          // ... once at most kTail blocks are left unclaimed
   constexpr int kTail = HOOD_STEAL_TAIL;
@@ -1583,6 +1586,13 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
       if (b >= 0) {
         issue(b, s_new);
         ++ci_b;
+#if HOOD_STEAL_PF
+        // the range's next block on its way into L2 (one 128-byte line per
+        // lane): a second block in flight per warp
+        const int pb = b + HOOD_STEAL_PF;
+        if (pb < nfull && pb < (ci_mode == 0 ? claimed_to : cs[2]))
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(gbytes + (long long)pb * BB + lane * 112));
+#endif
       }
     } else {
       if (ci.b < ci.e) issue(ci.b, s_new);
