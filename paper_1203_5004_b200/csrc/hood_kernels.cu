@@ -1078,8 +1078,9 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
   // (wr + j*512) ^ ((j & 1) << 6) (U == 8)
   const unsigned wr = U == 8 ? ring_s + (lane >> 3) * 128 + (((lane & 7) ^ (lane >> 3)) << 4)
                              : ring_s + (lane >> 2) * 64 + (((lane & 3) ^ ((lane >> 3) & 3)) << 4);
+  // ring slots are named by their byte offset in the warp's ring (s * BB)
   auto run_addr = [&](int l, int slot) -> unsigned {
-    return ring_s + slot * BB + l * (16 * U) + (ring_rot<U>(l) << 4);
+    return ring_s + slot + l * (16 * U) + (ring_rot<U>(l) << 4);
   };
   V* Hs = reinterpret_cast<V*>(wb + LY::HS);
   V* PBf = reinterpret_cast<V*>(wb + LY::PB);
@@ -1155,6 +1156,8 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
   int ci_mode = 0;              // 0 owner, 1 search, 2 stolen range, 3 done
   int ci_b = 0;                 // next block to issue
   int claimed_to = 0;           // owner: end of its claimed blocks
+  int ci_lim = 0;               // end of the issue cursor's range, at most nfull (prefetch limit)
+  const long long pf_off = (long long)HOOD_STEAL_PF * BB + lane * 112;  // lane's line of the prefetched block
   // cold state in smem (touched once per claim or range): [0] a claim in
   // flight, [1] blocks stolen from the owner's unit, [2] the stolen range's
   // end, [3] the size of the claim in flight
@@ -1247,6 +1250,7 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
           }
           if (cnt > 0) {
             claimed_to = own_b0 + f + cnt;
+            ci_lim = min(claimed_to, nfull);
             const int left = own_b1 - own_s - claimed_to;
             if (left > 0 && lane == 0) {
               const int g = left > kTail ? kG : kGs;  // small claims near the end: less to steal around
@@ -1278,6 +1282,7 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
           }
           __syncwarp();
           ci_b = sb;
+          ci_lim = min(se, nfull);
           ci_mode = 2;
           return ci_b;
         }
@@ -1318,7 +1323,7 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
 #endif
   auto issue = [&](int b, int s) {
     const long long off = (long long)b * BB;
-    const unsigned dst = wr + s * BB;
+    const unsigned dst = wr + s;
     if (b < nfull) {
 #pragma unroll
       for (int j = 0; j < U; ++j)
@@ -1426,6 +1431,7 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
     // the first pair of blocks is the owner's without a claim; the next
     // claim goes out at once
     claimed_to = min(own_b0 + kG, own_b1);
+    ci_lim = min(claimed_to, nfull);
     if (lane == 0) {
       // this build's epoch, nothing stolen, the first claim taken
       p.steal_w[own_u] = ((unsigned long long)p.steal_epoch << 48) | (unsigned long long)(claimed_to - own_b0);
@@ -1490,11 +1496,11 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
     if constexpr (STEAL) {
       const int b = ci_next();
       if (b >= 0) {
-        issue(b, s);
+        issue(b, s * BB);
         ++ci_b;
       }
     } else {
-      if (ci.b < ci.e) issue(ci.b, s);
+      if (ci.b < ci.e) issue(ci.b, s * BB);
     }
     cp_async_commit();
     if constexpr (!STEAL) advance(ci);
@@ -1535,7 +1541,7 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
     else cf_first = advance(cf);
   }
 #pragma unroll
-  for (int i = 0; i + 1 < D; ++i) land_next(i + 1, lmw[i], win[i]);
+  for (int i = 0; i + 1 < D; ++i) land_next((i + 1) * BB, lmw[i], win[i]);
   lmw[D - 1] = NEG;
   win[D - 1] = NEG;
   if (kTrace && p.trace && lane == 0) {
@@ -1555,9 +1561,9 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
   int pend = 0;     // queued survivors in PBf
   bool ht_ok = false;  // htail holds the hood's last two corners (set by a direct append)
   bool fresh = true;
-  int s_cur = 0;    // ring slot of sequence block k
-  int s_far = D;    // ring slot of block k + D
-  int s_new = D + P;  // ring slot of block k + D + P
+  int s_cur = 0;            // ring slot (byte offset) of sequence block k
+  int s_far = D * BB;       // ... of block k + D
+  int s_new = (D + P) * BB;  // ... of block k + D + P
 
   // fold the queued survivors (x order) into the running hood
   auto flush = [&]() {
@@ -1589,9 +1595,8 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
 #if HOOD_STEAL_PF
         // the range's next block on its way into L2 (one 128-byte line per
         // lane): a second block in flight per warp
-        const int pb = b + HOOD_STEAL_PF;
-        if (pb < nfull && pb < (ci_mode == 0 ? claimed_to : cs[2]))
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(gbytes + (long long)pb * BB + lane * 112));
+        if (b + HOOD_STEAL_PF < ci_lim)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(gbytes + (long long)b * BB + pf_off));
 #endif
       }
     } else {
@@ -1706,7 +1711,7 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
           // every point survives (arc-like input): straight to the output
           // slots when the block continues the hood as a concave chain
           flush();
-          const AppendRes ar = append_full_block<S, U, HC>(a, ring_s + s_cur * BB, Hs, gout + ubase, htail, hs, ht_ok);
+          const AppendRes ar = append_full_block<S, U, HC>(a, ring_s + s_cur, Hs, gout + ubase, htail, hs, ht_ok);
           hs = ar.h;
           appended = ar.ok;
           ht_ok = ar.ok;
@@ -1724,7 +1729,7 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
 #pragma unroll
         for (int k = 0; k < U; ++k) c[k] = lds16<L>(a ^ (k << 4));
         __syncwarp();
-        dst = reinterpret_cast<V*>(wring + (size_t)s_cur * BB);
+        dst = reinterpret_cast<V*>(wring + s_cur);
 #pragma unroll
         for (int i = 0; i < NP; ++i)
           if ((svm >> i) & 1u) dst[pos++] = pt_of(c[i / PPL], i % PPL);
@@ -1758,9 +1763,16 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
       lmw[i] = lmw[i + 1];
       win[i] = win[i + 1];
     }
-    s_cur = (s_cur + 1 == R) ? 0 : s_cur + 1;
-    s_far = (s_far + 1 == R) ? 0 : s_far + 1;
-    s_new = (s_new + 1 == R) ? 0 : s_new + 1;
+    if constexpr (R == 3 && D == 1) {  // the three slots rotate: register moves
+      const int t = s_cur;
+      s_cur = s_far;
+      s_far = s_new;
+      s_new = t;
+    } else {
+      s_cur = (s_cur + BB == R * BB) ? 0 : s_cur + BB;
+      s_far = (s_far + BB == R * BB) ? 0 : s_far + BB;
+      s_new = (s_new + BB == R * BB) ? 0 : s_new + BB;
+    }
 
     if (nrem == 0) {
       // unit done: its hood to the output slots, its summary for finalize
