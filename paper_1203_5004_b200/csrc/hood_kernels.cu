@@ -1101,9 +1101,11 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
   const int gw = blockIdx.x * (blockDim.x >> 5) + warp;
   const int nwarps = gridDim.x * (blockDim.x >> 5);
 
+  // unit numbers fit in 31 bits (make_plan)
+  const unsigned u_lo = (unsigned)p.unit_lo + (unsigned)gw, u_hi = (unsigned)p.unit_hi;
   auto seek = [&](UnitCur& c) {  // c.r set: load the block range of its unit
-    const long long u = p.unit_lo + gw + (long long)c.r * nwarps;
-    if (u < p.unit_hi) {
+    const unsigned u = u_lo + (unsigned)c.r * (unsigned)nwarps;
+    if (u < u_hi) {
       if (spi == 1) {
         c.b = (int)u * bpi;
         c.e = c.b + bpi;
@@ -1521,7 +1523,7 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
     if (STEAL ? svalid(cf) : cf.b < cf.e) {
       bool hp = true;
       if (cf_first) {
-        hp = (cf.b % bpi) != 0;
+        hp = spi != 1 && (cf.b % bpi) != 0;  // whole-instance units start their instance
         xcf = hp ? gpts[(long long)cf.b * BP - 1].x : NEG;
       }
       lm = land(cf.b, slot, hp, xcf);
@@ -1615,7 +1617,7 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
     if (fresh) {
       fresh = false;
       if constexpr (STEAL) u = qu[cc.r & 3];
-      else u = p.unit_lo + gw + (long long)cc.r * nwarps;
+      else u = (long long)(u_lo + (unsigned)cc.r * (unsigned)nwarps);
       inst = spi == 1 ? (int)u : (int)u / spi;
       ubase = (long long)cc.b * BP;
       // edge anchors: max y of up to EXT points on each side of the unit
