@@ -151,8 +151,20 @@ __device__ __forceinline__ float okey_inv(unsigned k) {
 }
 template <class S>
 __device__ __forceinline__ S warp_max_fast(S v) {
-  const float f = sizeof(S) == 4 ? (float)v : __double2float_rd((double)v);
-  return (S)okey_inv(__reduce_max_sync(0xffffffffu, okey(f)));
+  return (S)okey_inv(__reduce_max_sync(0xffffffffu, okey((float)v)));
+}
+// double: the REDUX runs on the order-preserving key of the high word (sign,
+// exponent, 20 mantissa bits), and the result is decoded as the smallest
+// double with the winning high word -- never above the true maximum (no
+// float conversions)
+template <>
+__device__ __forceinline__ double warp_max_fast<double>(double v) {
+  const unsigned hi = (unsigned)__double2hiint(v);
+  const unsigned k = hi ^ ((unsigned)((int)hi >> 31) | 0x80000000u);
+  const unsigned m = __reduce_max_sync(0xffffffffu, k);
+  if (m & 0x80000000u) return __hiloint2double((int)(m & 0x7fffffffu), 0);
+  const unsigned h = ~m;  // negative: the most negative double of that high word (-inf stays -inf)
+  return __hiloint2double((int)h, h == 0xfff00000u ? 0 : (int)0xffffffffu);
 }
 
 // x strictly increasing (and optionally inside (0,1)); on failure record
