@@ -21,3 +21,4 @@ unset HOOD_B200_LIB
 for c in 3 4; do timeout 600 ncu --metrics smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_executed_op_ffma_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,gpu__time_duration.sum -k regex:"ring_hull|finalize" --launch-skip 6 -c 2 python bench.py --config $c --steps 1 --warmup 3 --no-e2e --no-kernel-events --cpu-seconds 0.01 > gpurun_out/ev/ncu_dfma_c$c.log 2>&1; done
 python tools/steal_diag.py > gpurun_out/ev/steal_diag.log 2>&1
 python tools/time_dent.py > gpurun_out/ev/time_dent.log 2>&1
+bash tools/gpu_checked.sh
