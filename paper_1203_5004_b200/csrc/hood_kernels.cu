@@ -1188,6 +1188,11 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
   // sampled units (all of them when there are at most 32), one CAS; one L2
   // round trip per attempt, attempts repeated only when the CAS loses a race
   int s_seq = 0;  // samples taken so far
+  // trace build only: steals taken, the last one's start (globaltimer) and
+  // size, the end of the owner's own range, the last range's start / end /
+  // blocks / candidate blocks, the time spent merging parts
+  int tr_steals = 0, tr_last_k = 0, tr_rb = 0, tr_cand = 0;
+  unsigned long long tr_last_t = 0, tr_own_end = 0, tr_range_end = 0, tr_merge = 0, tr_rs = 0;
   auto steal = [&](int& sb, int& se, int& sv, int& sk) -> bool {
     const long long units = p.unit_hi - p.unit_lo;
     for (int attempt = 0; attempt < 4; ++attempt) {
@@ -1279,6 +1284,7 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
         }
         if (lane == 0 && cs[1]) qf[ci_r & 3] |= 2;  // the owner's range ends; it was stolen from
         __syncwarp();
+        if (kTrace) tr_own_end = gtimer();
         ci_mode = 1;
       }
       if (ci_mode == 1) {
@@ -1295,6 +1301,11 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
             cs[2] = se;
           }
           __syncwarp();
+          if (kTrace) {
+            ++tr_steals;
+            tr_last_t = gtimer();
+            tr_last_k = se - sb;
+          }
           ci_b = sb;
           ci_lim = min(se, nfull);
           ci_mode = 2;
@@ -1626,8 +1637,14 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
       HOOD_TOC(c_land);
     }
 
+    if (kTrace) ++tr_rb;
     if (fresh) {
       fresh = false;
+      if (kTrace) {
+        tr_rs = gtimer();
+        tr_rb = 1;
+        tr_cand = 0;
+      }
       if constexpr (STEAL) u = qu[cc.r & 3];
       else u = (long long)(u_lo + (unsigned)cc.r * (unsigned)nwarps);
       inst = spi == 1 ? (int)u : (int)u / spi;
@@ -1662,6 +1679,7 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
     // lane runs reaching tau (every run at an instance edge)
     const unsigned cm = tau != NEG ? __ballot_sync(FULL, !(lmc < tau)) : FULL;
     if (cm != 0) HOOD_COUNT(n_cand);
+    if (kTrace && cm != 0) ++tr_cand;
     HOOD_TIC();
     if (cm != 0 && cm != FULL && __popc(cm) <= 2) {
       // a few runs: re-read them point-per-lane, queue the survivors
@@ -1789,6 +1807,7 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
     }
 
     if (nrem == 0) {
+      if (kTrace) tr_range_end = gtimer();
       // unit done: its hood to the output slots, its summary for finalize
       bool written = false;
       if (hs.in_smem && hs.n == 0 && pend <= PC) {
@@ -1839,11 +1858,13 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
               if (i == part || __ldcg(p.part_cnt + kStealParts * u + i) >= 0) k = i;
             Merged acc{part == 0 ? hs.n : (long long)__ldcg(p.part_cnt + kStealParts * u),
                        part == 0 ? ubase : __ldcg(p.part_base + kStealParts * u)};
+            const unsigned long long tm0 = kTrace ? gtimer() : 0;
             for (int i = k; i >= 1; --i) {
               const long long qc = i == part ? hs.n : (long long)__ldcg(p.part_cnt + kStealParts * u + i);
               const long long qb_ = i == part ? ubase : __ldcg(p.part_base + kStealParts * u + i);
               acc = merge_parts<V>(gout, acc.base, acc.n, qb_, qc);
             }
+            if (kTrace) tr_merge += gtimer() - tm0;
             hs.n = acc.n;
             hs.in_smem = 0;
             ubase = acc.base;
@@ -1930,7 +1951,18 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
     unsigned smid;
     asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
     p.trace[1024 + 4 * gw + 2] = smid;
-#ifdef HOOD_RING_COUNTERS
+#ifndef HOOD_RING_COUNTERS
+    if (STEAL) {  // the caller's buffer holds 1024 + 12 * 8192 entries (tools/trace_ring.py)
+      p.trace[1024 + 4 * 8192 + 4 * gw] = tr_steals;
+      p.trace[1024 + 4 * 8192 + 4 * gw + 1] = (long long)tr_last_t;
+      p.trace[1024 + 4 * 8192 + 4 * gw + 2] = tr_last_k;
+      p.trace[1024 + 4 * 8192 + 4 * gw + 3] = (long long)tr_own_end;
+      p.trace[1024 + 8 * 8192 + 4 * gw] = (long long)tr_range_end;
+      p.trace[1024 + 8 * 8192 + 4 * gw + 1] = (long long)tr_merge;
+      p.trace[1024 + 8 * 8192 + 4 * gw + 2] = (long long)tr_rs;
+      p.trace[1024 + 8 * 8192 + 4 * gw + 3] = ((long long)tr_cand << 32) | tr_rb;
+    }
+#else
     p.trace[1024 + 4 * gw + 3] = ((long long)n_cand << 32) | (n_edge << 16) | n_many;
     p.trace[1024 + 4 * 8192 + 4 * gw] = c_cand;
     p.trace[1024 + 4 * 8192 + 4 * gw + 1] = c_flush;

@@ -16,7 +16,7 @@ from paper_1203_5004_b200 import workloads as W  # noqa: E402
 L = H.library()
 L.hood_internal_set_debug.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
 ctx = H.Context.get(0)
-trace = torch.zeros(1024 + 8 * 8192, dtype=torch.int64, device="cuda")
+trace = torch.zeros(1024 + 12 * 8192, dtype=torch.int64, device="cuda")
 flush = torch.empty(64 << 20, dtype=torch.int32, device="cuda")
 for lg in sys.argv[1:] or ["12", "16", "20", "22", "24"]:
     block = 0
@@ -64,10 +64,12 @@ for lg in sys.argv[1:] or ["12", "16", "20", "22", "24"]:
           + (f", ends +{(fin1 - t[0])/1e3:6.1f} us" if fin1 else "")
           + (f"; finalize CTA resident +{(finr - t[0])/1e3:6.1f} us" if finr else ""))
     w = trace[1024:1024 + 4 * 8192].view(-1, 4).cpu()
-    cyc = trace[1024 + 4 * 8192:].view(-1, 4).cpu()
+    cyc = trace[1024 + 4 * 8192:1024 + 8 * 8192].view(-1, 4).cpu()
+    ex2 = trace[1024 + 8 * 8192:].view(-1, 4).cpu()
     keep = w[:, 0] > 0
     w = w[keep]
     cyc = cyc[keep]
+    ex2 = ex2[keep]
     ent = (w[:, 0] - t[0]).double() / 1e3
     ext = (w[:, 1] - t[0]).double() / 1e3
     dur = ext - ent
@@ -95,6 +97,36 @@ for lg in sys.argv[1:] or ["12", "16", "20", "22", "24"]:
             bysm[int(w[i, 2])].append(float(dur[i]))
         means = sorted((sum(v) / len(v), k) for k, v in bysm.items())
         print("   SM mean duration: fastest", [(k, round(m, 1)) for m, k in means[:5]], "slowest", [(k, round(m, 1)) for m, k in means[-5:]])
+    if int(cyc[:, 0].abs().sum()) and int(cyc[:, 3].min()) > 1 << 40:  # STEAL kernel: steals per warp
+        nst = cyc[:, 0]
+        lt = (cyc[:, 1] - t[0]).double() / 1e3
+        lk = cyc[:, 2]
+        oe = (cyc[:, 3] - t[0]).double() / 1e3
+        order = torch.argsort(ext)
+        print(f"   steals per warp: mean {float(nst.double().mean()):.2f} max {int(nst.max())}; own range end q0/50/100: "
+              f"{float(oe.min()):.1f} {float(oe.median()):.1f} {float(oe.max()):.1f}")
+        re = (ex2[:, 0] - t[0]).double() / 1e3
+        mg = ex2[:, 1].double() / 1e3
+        print("   last 16 exits (exit, own range end, steals, last steal at, its blocks, last range's end, merge us):",
+              [(round(float(ext[i]), 1), round(float(oe[i]), 1), int(nst[i]), round(float(lt[i]), 1) if int(nst[i]) else None,
+                int(lk[i]), round(float(re[i]), 1), round(float(mg[i]), 1)) for i in order[-16:]])
+        print(f"   merge time per warp: mean {float(mg.mean()):.2f} us, max {float(mg.max()):.1f}; warps that merged: {int((mg > 0).sum())}")
+        rs = (ex2[:, 2] - t[0]).double() / 1e3
+        rb = (ex2[:, 3] & 0xffffffff).double()
+        rc = (ex2[:, 3] >> 32).double()
+        per = (re - rs) / rb.clamp(min=1)
+        th = nst > 0
+        print(f"   last range: us per block, thieves q50/90 {float(per[th].median()):.2f} {float(per[th].quantile(0.9)):.2f}; "
+              f"owners (unstolen last range) q50/90 {float(per[~th].median()):.2f} {float(per[~th].quantile(0.9)):.2f}")
+        print(f"   last range: candidate blocks per block, thieves {float((rc[th] / rb[th].clamp(min=1)).mean()):.3f}, "
+              f"owners {float((rc[~th] / rb[~th].clamp(min=1)).mean()):.3f}")
+        print("   last 16 exits (range start, blocks, us/block):", [(round(float(rs[i]), 1), int(rb[i]), round(float(per[i]), 2)) for i in order[-16:]])
+        print(f"   exit - last range end: q50 {float((ext - re).median()):.1f} q90 {float((ext - re).quantile(0.9)):.1f} max {float((ext - re).max()):.1f}")
+        thief = nst > 0
+        for nm, m in (("warps that stole", thief), ("warps that did not", ~thief)):
+            if int(m.sum()):
+                print(f"   {nm}: {int(m.sum())}, exit q50/90/100 {float(ext[m].median()):.1f} "
+                      f"{float(ext[m].quantile(0.9)):.1f} {float(ext[m].max()):.1f}")
     import collections
     persm = collections.defaultdict(list)
     for i in range(len(w)):
