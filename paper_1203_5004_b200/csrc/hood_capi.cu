@@ -1087,7 +1087,9 @@ int hood_last_error(hood_ctx* ctx, hood_error* out) {
 int hood_last_launch_count(hood_ctx* ctx) { return ctx ? ctx->last_launches : 0; }
 
 // Internal profiling hooks (not part of the public header): kernel debug
-// mode and a device buffer of 6*64 int64 for per-tile clock64 stamps of CTA 0.
+// mode (4: every odd ring warp held back 300 us, so the others steal) and,
+// for the -DHOOD_TRACE build only, a device buffer of 1024 + 12 * 8192 int64
+// for the kernels' stamps (tools/trace_ring.py, tools/trace_finalize.py).
 extern "C" int hood_internal_set_debug(hood_ctx* ctx, int mode, void* trace) {
   if (!ctx) return HOOD_ERR_INVALID_ARG;
   ctx->dbg = mode;

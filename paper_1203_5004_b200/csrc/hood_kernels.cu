@@ -38,8 +38,12 @@ namespace hood_b200 {
 // build carries none of it.
 #ifdef HOOD_TRACE
 constexpr bool kTrace = true;
+// per-warp trace records: warps [0, kTraceWarps) of the ring kernel, in a
+// buffer of 1024 + 12 * kTraceWarps entries (tools/trace_ring.py)
+constexpr int kTraceWarps = 8192;
 #else
 constexpr bool kTrace = false;
+constexpr int kTraceWarps = 8192;
 #endif
 
 // Bounds/invariant checks, compiled in only with -DHOOD_CHECKED (the checked
@@ -1436,7 +1440,7 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
   // profiling (p.trace, globaltimer ns): [0] first warp entry, [1] last warp
   // exit, [2] last prologue end; per warp gw at [1024 + 4 gw]: entry, exit, SM
   if (kTrace && p.trace && lane == 0) atomicMin(reinterpret_cast<unsigned long long*>(p.trace), gtimer());
-  if (kTrace && p.trace && lane == 0) p.trace[1024 + 4 * gw] = (long long)gtimer();
+  if (kTrace && p.trace && lane == 0 && gw < kTraceWarps) p.trace[1024 + 4 * gw] = (long long)gtimer();
 #ifdef HOOD_RING_COUNTERS
   int n_cand = 0, n_edge = 0, n_many = 0;
   long long c_cand = 0, c_flush = 0, c_land = 0;
@@ -1573,7 +1577,7 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
     const unsigned long long t = gtimer();
     atomicMax(reinterpret_cast<unsigned long long*>(p.trace) + 2, t);
 #ifndef HOOD_RING_COUNTERS
-    p.trace[1024 + 4 * gw + 3] = (long long)t;  // this warp's prologue end
+    if (gw < kTraceWarps) p.trace[1024 + 4 * gw + 3] = (long long)t;  // this warp's prologue end
 #endif
   }
 
@@ -1946,13 +1950,13 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
   }
   cp_async_wait<0>();
   if (kTrace && p.trace && lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(p.trace) + 1, gtimer());
-  if (kTrace && p.trace && lane == 0) {
+  if (kTrace && p.trace && lane == 0 && gw < kTraceWarps) {
     p.trace[1024 + 4 * gw + 1] = (long long)gtimer();
     unsigned smid;
     asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
     p.trace[1024 + 4 * gw + 2] = smid;
 #ifndef HOOD_RING_COUNTERS
-    if (STEAL) {  // the caller's buffer holds 1024 + 12 * 8192 entries (tools/trace_ring.py)
+    if (STEAL) {
       p.trace[1024 + 4 * 8192 + 4 * gw] = tr_steals;
       p.trace[1024 + 4 * 8192 + 4 * gw + 1] = (long long)tr_last_t;
       p.trace[1024 + 4 * 8192 + 4 * gw + 2] = tr_last_k;
