@@ -1026,10 +1026,10 @@ def _steal_lib():
 @pytest.mark.parametrize("shape", ["gauss26", "arc25", "dent25", "multi"])
 def test_tail_stealing_parity(oracle_mod, shape):
     """Work stealing of unit tails (the STEAL ring kernel): with every odd
-    warp held back 300 us (debug mode 4) the others steal the back halves of
-    those units, the two parts of each stolen unit are merged by bridge +
-    splice, and the hood is still the oracle's, bit for bit -- single builds,
-    multi-instance builds and the chunked host path."""
+    warp held back 300 us (debug mode 4) the others steal from those units
+    (up to three times each), the parts of each stolen unit are merged left
+    to right by bridge + splice, and the hood is still the oracle's, bit for
+    bit -- single builds, multi-instance builds and the chunked host path."""
     L = _steal_lib()
     ctx = H.Context.get(0)
     rng = np.random.default_rng(7)
@@ -1064,6 +1064,11 @@ def test_tail_stealing_parity(oracle_mod, shape):
     finally:
         L.hood_internal_set_debug(ctx.handle, 0, None)
     assert steals > 0, shape
+    if not block:
+        # several steals per unit (up to kStealParts - 1 = 3): more steals than
+        # delayed units (every odd warp of 3 CTAs x 4 warps per SM), so
+        # merges of three and four parts ran too
+        assert steals > torch.cuda.get_device_properties(0).multi_processor_count * 6, (shape, steals)
     # and the normal mode after it: the claim words of the slowed build
     # never leak into the next one
     assert same(H.build_hood(t, block_len=block).counts.cpu().numpy(), rep.counts.cpu().numpy())
