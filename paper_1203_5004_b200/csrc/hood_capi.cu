@@ -1088,7 +1088,7 @@ int hood_last_launch_count(hood_ctx* ctx) { return ctx ? ctx->last_launches : 0;
 
 // Internal profiling hooks (not part of the public header): kernel debug
 // mode (4: every odd ring warp held back 300 us, so the others steal) and,
-// for the -DHOOD_TRACE build only, a device buffer of 1024 + 12 * 8192 int64
+// for the -DHOOD_TRACE build only, a device buffer of 1024 + 16 * 8192 int64
 // for the kernels' stamps (tools/trace_ring.py, tools/trace_finalize.py).
 extern "C" int hood_internal_set_debug(hood_ctx* ctx, int mode, void* trace) {
   if (!ctx) return HOOD_ERR_INVALID_ARG;

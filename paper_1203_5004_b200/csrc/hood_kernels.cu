@@ -39,7 +39,7 @@ namespace hood_b200 {
 #ifdef HOOD_TRACE
 constexpr bool kTrace = true;
 // per-warp trace records: warps [0, kTraceWarps) of the ring kernel, in a
-// buffer of 1024 + 12 * kTraceWarps entries (tools/trace_ring.py)
+// buffer of 1024 + 16 * kTraceWarps entries (tools/trace_ring.py)
 constexpr int kTraceWarps = 8192;
 #else
 constexpr bool kTrace = false;
@@ -1175,6 +1175,8 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
   int ci_b = 0;                 // next block to issue
   int claimed_to = 0;           // owner: end of its claimed blocks
   int ci_lim = 0;               // end of the issue cursor's range, at most nfull (prefetch limit)
+  int ci_hi = 0;                // blocks below it are issued without ci_next (the owner's claimed
+                                // blocks, a stolen range; 0 while searching)
   const long long pf_off = (long long)HOOD_STEAL_PF * BB + lane * 112;  // lane's line of the prefetched block
   // cold state in smem (touched once per claim or range): [0] a claim in
   // flight, [1] blocks stolen from the owner's unit, [2] the stolen range's
@@ -1195,7 +1197,8 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
   // trace build only: steals taken, the last one's start (globaltimer) and
   // size, the end of the owner's own range, the last range's start / end /
   // blocks / candidate blocks, the time spent merging parts
-  int tr_steals = 0, tr_last_k = 0, tr_rb = 0, tr_cand = 0;
+  int tr_steals = 0, tr_last_k = 0, tr_rb = 0, tr_cand = 0, tr_nb = 0;
+  unsigned long long tr_t[4] = {0, 0, 0, 0};  // when the warp had processed 128, 256, 384, 512 blocks
   unsigned long long tr_last_t = 0, tr_own_end = 0, tr_range_end = 0, tr_merge = 0, tr_rs = 0;
   auto steal = [&](int& sb, int& se, int& sv, int& sk) -> bool {
     const long long units = p.unit_hi - p.unit_lo;
@@ -1274,6 +1277,7 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
           if (cnt > 0) {
             claimed_to = own_b0 + f + cnt;
             ci_lim = min(claimed_to, nfull);
+            ci_hi = claimed_to;
             const int left = own_b1 - own_s - claimed_to;
             if (left > 0 && lane == 0) {
               const int g = left > kTail ? kG : kGs;  // small claims near the end: less to steal around
@@ -1289,6 +1293,7 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
         if (lane == 0 && cs[1]) qf[ci_r & 3] |= 2;  // the owner's range ends; it was stolen from
         __syncwarp();
         if (kTrace) tr_own_end = gtimer();
+        ci_hi = 0;
         ci_mode = 1;
       }
       if (ci_mode == 1) {
@@ -1312,6 +1317,7 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
           }
           ci_b = sb;
           ci_lim = min(se, nfull);
+          ci_hi = se;
           ci_mode = 2;
           return ci_b;
         }
@@ -1319,6 +1325,7 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
       }
       if (ci_mode == 2) {
         if (ci_b < cs[2]) return ci_b;
+        ci_hi = 0;
         ci_mode = 1;
         continue;
       }
@@ -1461,6 +1468,7 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
     // claim goes out at once
     claimed_to = min(own_b0 + kG, own_b1);
     ci_lim = min(claimed_to, nfull);
+    ci_hi = claimed_to;
     if (lane == 0) {
       // this build's epoch, nothing stolen, the first claim taken
       p.steal_w[own_u] = ((unsigned long long)p.steal_epoch << 48) | (unsigned long long)(claimed_to - own_b0);
@@ -1617,7 +1625,7 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
   while (STEAL ? svalid(cc) : cc.b < cc.e) {
     // keep P blocks in flight: issue k+D+P, then block k+D has landed
     if constexpr (STEAL) {
-      const int b = (ci_mode == 0 && ci_b < claimed_to) ? ci_b : ci_next();
+      const int b = ci_b < ci_hi ? ci_b : ci_next();
       if (b >= 0) {
         issue(b, s_new);
         ++ci_b;
@@ -1641,7 +1649,11 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
       HOOD_TOC(c_land);
     }
 
-    if (kTrace) ++tr_rb;
+    if (kTrace) {
+      ++tr_rb;
+      ++tr_nb;
+      if ((tr_nb & 127) == 0 && tr_nb <= 512) tr_t[(tr_nb >> 7) - 1] = gtimer();
+    }
     if (fresh) {
       fresh = false;
       if (kTrace) {
@@ -1965,6 +1977,7 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
       p.trace[1024 + 8 * 8192 + 4 * gw + 1] = (long long)tr_merge;
       p.trace[1024 + 8 * 8192 + 4 * gw + 2] = (long long)tr_rs;
       p.trace[1024 + 8 * 8192 + 4 * gw + 3] = ((long long)tr_cand << 32) | tr_rb;
+      for (int i = 0; i < 4; ++i) p.trace[1024 + 12 * 8192 + 4 * gw + i] = (long long)tr_t[i];
     }
 #else
     p.trace[1024 + 4 * gw + 3] = ((long long)n_cand << 32) | (n_edge << 16) | n_many;

@@ -21,7 +21,7 @@ pts = W.grid_uniform_torch(n, seed=2) if cfg == 2 else (W.arc_torch(n) if cfg ==
 L = H.library()
 L.hood_internal_set_debug.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
 ctx = H.Context.get(0)
-trace = torch.zeros(1024 + 12 * 8192, dtype=torch.int64, device="cuda")
+trace = torch.zeros(1024 + 16 * 8192, dtype=torch.int64, device="cuda")
 corners = torch.empty_like(pts)
 counts = torch.empty(1, dtype=torch.int32, device="cuda")
 for rep in range(5):

@@ -16,7 +16,7 @@ from paper_1203_5004_b200 import workloads as W  # noqa: E402
 L = H.library()
 L.hood_internal_set_debug.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
 ctx = H.Context.get(0)
-trace = torch.zeros(1024 + 12 * 8192, dtype=torch.int64, device="cuda")
+trace = torch.zeros(1024 + 16 * 8192, dtype=torch.int64, device="cuda")
 flush = torch.empty(64 << 20, dtype=torch.int32, device="cuda")
 for lg in sys.argv[1:] or ["12", "16", "20", "22", "24"]:
     block = 0
@@ -65,11 +65,13 @@ for lg in sys.argv[1:] or ["12", "16", "20", "22", "24"]:
           + (f"; finalize CTA resident +{(finr - t[0])/1e3:6.1f} us" if finr else ""))
     w = trace[1024:1024 + 4 * 8192].view(-1, 4).cpu()
     cyc = trace[1024 + 4 * 8192:1024 + 8 * 8192].view(-1, 4).cpu()
-    ex2 = trace[1024 + 8 * 8192:].view(-1, 4).cpu()
+    ex2 = trace[1024 + 8 * 8192:1024 + 12 * 8192].view(-1, 4).cpu()
+    ex3 = trace[1024 + 12 * 8192:].view(-1, 4).cpu()
     keep = w[:, 0] > 0
     w = w[keep]
     cyc = cyc[keep]
     ex2 = ex2[keep]
+    ex3 = ex3[keep]
     ent = (w[:, 0] - t[0]).double() / 1e3
     ext = (w[:, 1] - t[0]).double() / 1e3
     dur = ext - ent
@@ -118,6 +120,21 @@ for lg in sys.argv[1:] or ["12", "16", "20", "22", "24"]:
         th = nst > 0
         print(f"   last range: us per block, thieves q50/90 {float(per[th].median()):.2f} {float(per[th].quantile(0.9)):.2f}; "
               f"owners (unstolen last range) q50/90 {float(per[~th].median()):.2f} {float(per[~th].quantile(0.9)):.2f}")
+        ok = (ex3[:, 3] > 0)
+        if int(ok.sum()):
+            tt = (ex3[ok].double() - t[0]) / 1e3
+            en = ent[ok]
+            r0 = (tt[:, 0] - en) / 128
+            rr = [(tt[:, j + 1] - tt[:, j]) / 128 for j in range(3)]
+            print(f"   us per block by phase (warps with >= 512 blocks, {int(ok.sum())}): blocks 0-127 {float(r0.median()):.3f}, "
+                  + ", ".join(f"{128 * (j + 1)}-{128 * (j + 2) - 1} {float(r.median()):.3f}" for j, r in enumerate(rr))
+                  + f"; at {float(tt[:, 3].median()):.0f} us")
+            late = ok & (nst == 0) & (rb > 530)
+            if int(late.sum()):
+                t512 = (ex3[late][:, 3].double() - t[0]) / 1e3
+                rl = (re[late] - t512) / (rb[late] - 512)
+                print(f"   warps that never stole, blocks 512..end of their unit ({int(late.sum())}): "
+                      f"{float(rl.median()):.3f} us per block (q90 {float(rl.quantile(0.9)):.3f}), ending at {float(re[late].median()):.0f} us")
         print(f"   last range: candidate blocks per block, thieves {float((rc[th] / rb[th].clamp(min=1)).mean()):.3f}, "
               f"owners {float((rc[~th] / rb[~th].clamp(min=1)).mean()):.3f}")
         print("   last 16 exits (range start, blocks, us/block):", [(round(float(rs[i]), 1), int(rb[i]), round(float(per[i]), 2)) for i in order[-16:]])
