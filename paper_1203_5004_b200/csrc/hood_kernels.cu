@@ -1652,7 +1652,12 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
     if (kTrace) {
       ++tr_rb;
       ++tr_nb;
+#ifdef HOOD_TRACE_EARLY  // tools/trace_early.py: the early blocks' rates
+      if (tr_nb == 16 || tr_nb == 64 || tr_nb == 128 || tr_nb == 256)
+        tr_t[tr_nb == 16 ? 0 : tr_nb == 64 ? 1 : tr_nb == 128 ? 2 : 3] = gtimer();
+#else
       if ((tr_nb & 127) == 0 && tr_nb <= 512) tr_t[(tr_nb >> 7) - 1] = gtimer();
+#endif
     }
     if (fresh) {
       fresh = false;
