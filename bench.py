@@ -181,6 +181,22 @@ def cpu_reference_rate(points_np, seconds: float, threads: int):
     return pts.shape[0] / statistics.median(times) / 1e9, kind, len(times)
 
 
+def psim_build_hood_rate(points_np):
+    """Gpoints/s of the reference's own hood::build_hood round loop (psim, the
+    simulated CUDA launches of driver.cpp:20-43 without validate_points, which
+    rejects random inputs from 2^16 on: SURVEY A4), one run, single thread."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    import numpy as np
+    pts = np.ascontiguousarray(points_np, dtype=np.float64)
+    t0 = time.perf_counter()
+    O.ref_build_hood_raw(pts)
+    dt = time.perf_counter() - t0
+    return {"value": pts.shape[0] / dt / 1e9, "unit": UNIT, "cores": 1, "ms": dt * 1e3,
+            "what": "the reference's hood::build_hood round loop (psim: log2 n - 1 rounds of the 9-phase "
+                    "match_and_merge kernel on the CPU), the path the drop-in replaces; oracle/_ref, same input"}
+
+
 def cpu_reference_batched_rate(points_np, block, seconds, threads):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
@@ -549,12 +565,19 @@ def run_ours(args):
                 rate, kind, reps = cpu_reference_batched_rate(hostpts, block, args.cpu_seconds, 1)
             else:
                 rate, kind, reps = cpu_reference_rate(hostpts, args.cpu_seconds, 1)
-            del hostpts
             cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": kind, "cpu_model": cpu_model(),
                    "host_threads": os.cpu_count(),
                    "sample": f"full workload ({n} points) x {reps} runs (median), "
                              f"{'oracle/_ref = reference oracle::upper_hull' if kind == 'reference' else 'C port'}"
                              f", single thread, same input"}
+            if not block and n <= (1 << 16) and kind == "reference":
+                # the path the drop-in replaces, hood::build_hood's round loop
+                # (psim), timed where it finishes in seconds (SURVEY 8(d) iv)
+                try:
+                    cpu["reference_build_hood"] = psim_build_hood_rate(hostpts)
+                except RuntimeError as e:  # DegenerateTangent on this input
+                    cpu["reference_build_hood"] = {"unavailable": str(e)}
+            del hostpts
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
