@@ -747,17 +747,20 @@ __device__ __noinline__ unsigned edge_survivors(unsigned a, long long q0, long l
 #pragma unroll
     for (int i = NP - 1; i >= 0; --i) {
       const S y = yv[i];
-      svm |= ((y != NEG && !(y < fmin(lft[i], Q))) ? 1u : 0u) << i;
+      svm |= (!(y < fmin(lft[i], Q)) ? 1u : 0u) << i;
       Q = fmax(Q, y);
     }
   } else {
 #pragma unroll
     for (int i = 0; i < NP; ++i) {
       const S y = yv[i];
-      svm |= ((y != NEG && !(y < fmin(lft[i], right))) ? 1u : 0u) << i;
+      svm |= (!(y < fmin(lft[i], right)) ? 1u : 0u) << i;
     }
   }
-  return svm;
+  // the points past the input's end (the padding of its last run) never
+  // survive: one mask, not a test per point
+  const long long nv = n - q0;
+  return nv >= NP ? svm : (nv <= 0 ? 0u : svm & ((1u << nv) - 1u));
 }
 
 // validate_points' collinearity margin over consecutive triples
