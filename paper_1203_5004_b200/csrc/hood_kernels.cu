@@ -642,6 +642,20 @@ __device__ __forceinline__ S scan_down_max(S v, int lane) {
   return v;
 }
 
+// Exclusive warp max-scans (toward higher / lower lanes), ident at the ends.
+template <class S>
+__device__ __forceinline__ S excl_up_max(S v, int lane, S ident) {
+  const S incl = scan_up_max(v, lane);
+  const S e = __shfl_up_sync(0xffffffffu, incl, 1);
+  return lane == 0 ? ident : e;
+}
+template <class S>
+__device__ __forceinline__ S excl_down_max(S v, int lane, S ident) {
+  const S incl = scan_down_max(v, lane);
+  const S e = __shfl_down_sync(0xffffffffu, incl, 1);
+  return lane == 31 ? ident : e;
+}
+
 __device__ __forceinline__ void cp_async16s(unsigned dst, const void* gsrc, int src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(gsrc), "r"(src_bytes) : "memory");
 }
@@ -1624,6 +1638,71 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
     HOOD_TOC(c_flush);
   };
 
+  // An instance-edge block (no block anchor on one side), transposed: the
+  // lane run maxima (landing pass) with exclusive lane scans bound every
+  // run's per-point anchors from below, so only the runs that can hold a
+  // survivor are read -- 32 / NP runs at a time, one point per lane, with
+  // segmented in-run scans for the exact per-point anchors (the same anchors
+  // edge_survivors uses) -- and their survivors are queued in x order.
+  // Returns false (nothing done) when too many runs qualify (arc-like
+  // input); edge_survivors then takes the whole block.  LEAN (batched)
+  // kernels only: there every block is an instance edge; in the others two
+  // blocks per build are, and the extra code costs them registers.
+  auto edge_runs = [&](long long bs, S right) -> bool {
+    constexpr int G = 32 / NP;  // runs per pass
+    const S lo_l = runmax == NEG ? excl_up_max<S>(lmc, lane, NEG) : runmax;
+    const S lo_r = right == NEG ? excl_down_max<S>(lmc, lane, NEG) : right;
+    unsigned qm = __ballot_sync(FULL, !(lmc < ymin<S>(lo_l, lo_r)));
+    if (__popc(qm) > 4 * G) return false;
+    const int j = lane % NP, g = lane / NP;
+    while (qm) {
+      unsigned mm = qm;
+#pragma unroll
+      for (int k = 0; k < G - 1; ++k)
+        if (k < g) mm &= mm - 1;
+      const int l = mm ? __ffs(mm) - 1 : -1;  // this lane's run
+#pragma unroll
+      for (int k = 0; k < G; ++k) qm &= qm - 1;
+      V q = make_vec<V>(NEG, NEG);
+      bool valid = false;
+      if (l >= 0) {
+        valid = bs + (long long)l * NP + j < n;
+        q = lds_pt((run_addr(l, s_cur) ^ ((j / PPL) << 4)) + (j % PPL) * (unsigned)sizeof(V), (V*)nullptr);
+      }
+      const S y = valid ? q.y : NEG;
+      const int src = l < 0 ? lane : l;
+      S lft = runmax, qr = right;
+      if (runmax == NEG) {  // prefix max before the point: lanes before the run, then the run
+        S v = y;
+#pragma unroll
+        for (int d = 1; d < NP; d <<= 1) {
+          const S o = __shfl_up_sync(FULL, v, d);
+          if (j >= d) v = ymax<S>(v, o);
+        }
+        const S e = __shfl_up_sync(FULL, v, 1);
+        const S el = __shfl_sync(FULL, lo_l, src);
+        lft = j == 0 ? el : ymax<S>(el, e);
+      }
+      if (right == NEG) {  // suffix max after the point
+        S v = y;
+#pragma unroll
+        for (int d = 1; d < NP; d <<= 1) {
+          const S o = __shfl_down_sync(FULL, v, d);
+          if (j + d < NP) v = ymax<S>(v, o);
+        }
+        const S e = __shfl_down_sync(FULL, v, 1);
+        const S er = __shfl_sync(FULL, lo_r, src);
+        qr = j == NP - 1 ? er : ymax<S>(er, e);
+      }
+      const bool sv = valid && !(y < fmin(lft, qr));
+      const unsigned bm = __ballot_sync(FULL, sv);
+      if (pend + __popc(bm) > PC) flush();
+      if (sv) PBf[pend + __popc(bm & below)] = q;
+      pend += __popc(bm);
+    }
+    return true;
+  };
+
 #pragma unroll 1
   while (STEAL ? svalid(cc) : cc.b < cc.e) {
     // keep P blocks in flight: issue k+D+P, then block k+D has landed
@@ -1723,7 +1802,7 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
         if (sv) PBf[pend + __popc(sm & below)] = q;  // room: pend <= PC - 2 NP here
         pend += __popc(sm);
       }
-    } else if (cm != 0) {
+    } else if (cm != 0 && !(LEAN && tau == NEG && edge_runs(bs, right))) {
       // many runs (arc-like input) or an instance edge (exact per-point
       // anchors on the side(s) without a block anchor): the whole block
       if (tau == NEG) HOOD_COUNT(n_edge);
