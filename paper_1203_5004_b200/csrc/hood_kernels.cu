@@ -1649,12 +1649,12 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
   // kernels only: there every block is an instance edge; in the others two
   // blocks per build are, and the extra code costs them registers.
   auto edge_runs = [&](long long bs, S right) -> bool {
-    constexpr int G = 32 / NP;  // runs per pass
+    constexpr int G = 32 / U;  // runs per pass: a run per U lanes, one 16-byte chunk (PPL points) per lane
     const S lo_l = runmax == NEG ? excl_up_max<S>(lmc, lane, NEG) : runmax;
     const S lo_r = right == NEG ? excl_down_max<S>(lmc, lane, NEG) : right;
     unsigned qm = __ballot_sync(FULL, !(lmc < ymin<S>(lo_l, lo_r)));
-    if (__popc(qm) > 4 * G) return false;
-    const int j = lane % NP, g = lane / NP;
+    if (__popc(qm) > 2 * G) return false;
+    const int j = lane % U, g = lane / U;
     while (qm) {
       unsigned mm = qm;
 #pragma unroll
@@ -1663,42 +1663,80 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
       const int l = mm ? __ffs(mm) - 1 : -1;  // this lane's run
 #pragma unroll
       for (int k = 0; k < G; ++k) qm &= qm - 1;
-      V q = make_vec<V>(NEG, NEG);
-      bool valid = false;
-      if (l >= 0) {
-        valid = bs + (long long)l * NP + j < n;
-        q = lds_pt((run_addr(l, s_cur) ^ ((j / PPL) << 4)) + (j % PPL) * (unsigned)sizeof(V), (V*)nullptr);
-      }
-      const S y = valid ? q.y : NEG;
-      const int src = l < 0 ? lane : l;
-      S lft = runmax, qr = right;
-      if (runmax == NEG) {  // prefix max before the point: lanes before the run, then the run
-        S v = y;
+      V q[PPL];
+      S y[PPL];
+      bool valid[PPL];
+      {
+        L c{};
+        if (l >= 0) c = lds16<L>(run_addr(l, s_cur) ^ (j << 4));
+        const long long i0 = bs + (long long)l * NP + j * PPL;
 #pragma unroll
-        for (int d = 1; d < NP; d <<= 1) {
+        for (int e = 0; e < PPL; ++e) {
+          q[e] = pt_of(c, e);
+          valid[e] = l >= 0 && i0 + e < n;
+          y[e] = valid[e] ? q[e].y : NEG;
+        }
+      }
+      const int src = l < 0 ? lane : l;
+      S lft[PPL], qr[PPL];
+#pragma unroll
+      for (int e = 0; e < PPL; ++e) {
+        lft[e] = runmax;
+        qr[e] = right;
+      }
+      if (runmax == NEG) {  // prefix max before each point: lanes before the run, the run's earlier chunks, the chunk
+        S v = y[0];
+#pragma unroll
+        for (int e = 1; e < PPL; ++e) v = ymax<S>(v, y[e]);
+#pragma unroll
+        for (int d = 1; d < U; d <<= 1) {
           const S o = __shfl_up_sync(FULL, v, d);
           if (j >= d) v = ymax<S>(v, o);
         }
-        const S e = __shfl_up_sync(FULL, v, 1);
+        const S ex = __shfl_up_sync(FULL, v, 1);
         const S el = __shfl_sync(FULL, lo_l, src);
-        lft = j == 0 ? el : ymax<S>(el, e);
-      }
-      if (right == NEG) {  // suffix max after the point
-        S v = y;
+        S run = j == 0 ? el : ymax<S>(el, ex);
 #pragma unroll
-        for (int d = 1; d < NP; d <<= 1) {
-          const S o = __shfl_down_sync(FULL, v, d);
-          if (j + d < NP) v = ymax<S>(v, o);
+        for (int e = 0; e < PPL; ++e) {
+          lft[e] = run;
+          run = ymax<S>(run, y[e]);
         }
-        const S e = __shfl_down_sync(FULL, v, 1);
-        const S er = __shfl_sync(FULL, lo_r, src);
-        qr = j == NP - 1 ? er : ymax<S>(er, e);
       }
-      const bool sv = valid && !(y < fmin(lft, qr));
-      const unsigned bm = __ballot_sync(FULL, sv);
-      if (pend + __popc(bm) > PC) flush();
-      if (sv) PBf[pend + __popc(bm & below)] = q;
-      pend += __popc(bm);
+      if (right == NEG) {  // suffix max after each point
+        S v = y[0];
+#pragma unroll
+        for (int e = 1; e < PPL; ++e) v = ymax<S>(v, y[e]);
+#pragma unroll
+        for (int d = 1; d < U; d <<= 1) {
+          const S o = __shfl_down_sync(FULL, v, d);
+          if (j + d < U) v = ymax<S>(v, o);
+        }
+        const S ex = __shfl_down_sync(FULL, v, 1);
+        const S er = __shfl_sync(FULL, lo_r, src);
+        S run = j == U - 1 ? er : ymax<S>(er, ex);
+#pragma unroll
+        for (int e = PPL - 1; e >= 0; --e) {
+          qr[e] = run;
+          run = ymax<S>(run, y[e]);
+        }
+      }
+      bool sv[PPL];
+      unsigned bm[PPL];
+      int before = 0, tot = 0;
+#pragma unroll
+      for (int e = 0; e < PPL; ++e) {
+        sv[e] = valid[e] && !(y[e] < fmin(lft[e], qr[e]));
+        bm[e] = __ballot_sync(FULL, sv[e]);
+        before += __popc(bm[e] & below);
+        tot += __popc(bm[e]);
+      }
+      if (pend + tot > PC) flush();
+#pragma unroll
+      for (int e = 0; e < PPL; ++e) {
+        if (sv[e]) PBf[pend + before] = q[e];
+        before += sv[e];
+      }
+      pend += tot;
     }
     return true;
   };
