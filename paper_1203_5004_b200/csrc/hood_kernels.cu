@@ -1625,7 +1625,9 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
     if (pend == 0) return;
     ht_ok = false;
     HOOD_TIC();
-    if (hs.in_smem && hs.n + pend <= HC) {  // pend <= PC: one lane pushes them
+    // pend <= PC: one lane pushes them; a large LEAN batch (arc-like edge
+    // blocks) goes to the warp's concave-append path instead
+    if (hs.in_smem && hs.n + pend <= HC && (!LEAN || pend < 32)) {
       long long h = hs.n;
       if (lane == 0) h = fold_linear<V>(PBf, pend, Hs, h);
       hs.n = __shfl_sync(FULL, h, 0);
@@ -1653,7 +1655,10 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
     const S lo_l = runmax == NEG ? excl_up_max<S>(lmc, lane, NEG) : runmax;
     const S lo_r = right == NEG ? excl_down_max<S>(lmc, lane, NEG) : right;
     unsigned qm = __ballot_sync(FULL, !(lmc < ymin<S>(lo_l, lo_r)));
-    if (__popc(qm) > 2 * G) return false;
+#ifndef HOOD_EDGE_PASSES
+#define HOOD_EDGE_PASSES 7  // passes at most; beyond (arc-like): edge_survivors and its batch merge
+#endif
+    if (__popc(qm) > HOOD_EDGE_PASSES * G) return false;
     const int j = lane % U, g = lane / U;
     while (qm) {
       unsigned mm = qm;
