@@ -777,6 +777,43 @@ __device__ __noinline__ unsigned edge_survivors(unsigned a, long long q0, long l
   return nv >= NP ? svm : (nv <= 0 ? 0u : svm & ((1u << nv) - 1u));
 }
 
+// An instance-edge block of a LEAN kernel with more than 28 qualifying runs
+// (arc-like): every point's exact anchors (edge_survivors), the survivors
+// compacted in place into the block's own slot (a survivor never lands past
+// its source) and merged into the hood as one batch.  Out of line so the
+// batched kernel's main loop keeps none of this code.
+template <class S, int U, int HC>
+__device__ __noinline__ HoodState lean_edge_block(unsigned a, typename PointT<S>::V* slot, long long q0, long long n,
+                                                  S runmax, S right, typename PointT<S>::V* Hs,
+                                                  typename PointT<S>::V* gslab, HoodState h) {
+  using V = typename PointT<S>::V;
+  using L = typename Ld16<S>::T;
+  constexpr int PPL = Ld16<S>::PPL, NP = U * PPL;
+  const int lane = threadIdx.x & 31;
+  const unsigned svm = edge_survivors<S, U>(a, q0, n, runmax, right);
+  const int cnt = __popc(svm);
+  int incl = cnt;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int o = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += o;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  L c[U];
+#pragma unroll
+  for (int k = 0; k < U; ++k) c[k] = lds16<L>(a ^ (k << 4));
+  __syncwarp();
+  int pos = incl - cnt;
+#pragma unroll
+  for (int i = 0; i < NP; ++i)
+    if ((svm >> i) & 1u) slot[pos++] = pt_of(c[i / PPL], i % PPL);
+  __syncwarp();
+  if (total > 0) h = merge_block_lean<S, HC>(slot, total, Hs, gslab, h);
+  __syncwarp();
+  return h;
+}
+
+
 // validate_points' collinearity margin over consecutive triples
 // (hoodbuf.cpp:16-26 check_triple, :59 the i, i+1, i+2 loop; hoodbuf.hpp:16
 // kCollinearMargin = 1e-9): |orient(p_k, p_i, p_j)| < 1e-9 for
@@ -1655,10 +1692,13 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
     const S lo_l = runmax == NEG ? excl_up_max<S>(lmc, lane, NEG) : runmax;
     const S lo_r = right == NEG ? excl_down_max<S>(lmc, lane, NEG) : right;
     unsigned qm = __ballot_sync(FULL, !(lmc < ymin<S>(lo_l, lo_r)));
-#ifndef HOOD_EDGE_PASSES
-#define HOOD_EDGE_PASSES 7  // passes at most; beyond (arc-like): edge_survivors and its batch merge
-#endif
-    if (__popc(qm) > HOOD_EDGE_PASSES * G) return false;
+    if (__popc(qm) > 7 * G) {  // arc-like: edge_survivors and one batch merge, out of line
+      flush();
+      hs = lean_edge_block<S, U, HC>(run_addr(lane, s_cur), reinterpret_cast<V*>(wring + s_cur), bs + lane * NP, n,
+                                     runmax, right, Hs, gout + ubase, hs);
+      ht_ok = false;
+      return true;
+    }
     const int j = lane % U, g = lane / U;
     while (qm) {
       unsigned mm = qm;
