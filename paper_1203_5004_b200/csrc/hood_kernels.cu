@@ -472,6 +472,33 @@ __device__ __forceinline__ int warp_hull_small(const V* P, int m, V* dst) {
   return __popcll(alive);
 }
 
+// warp_hull_small for m <= 32 points: one point per lane, 32-bit masks, one
+// ballot per round; an uncertain predicate hands the set to warp_hull_small
+// (whose reference-order chain decides).
+template <class V>
+__device__ __forceinline__ int warp_hull_small32(const V* P, int m, V* dst) {
+  const int lane = threadIdx.x & 31;
+  const V q = lane < m ? P[lane] : V{};
+  unsigned alive = m >= 32 ? ~0u : ((1u << m) - 1u);
+  bool unc = false;
+  for (;;) {
+    bool k = false;
+    if ((alive >> lane) & 1u) {
+      const unsigned lo = alive & ((1u << lane) - 1u);
+      const unsigned hi = alive & ~((2u << lane) - 1u);  // lane 31: 2u << 31 == 0, hi = 0
+      k = (!lo || !hi) ? true : above_flag(P[31 - __clz(lo)], q, P[__ffs(hi) - 1], unc);
+    }
+    const unsigned nxt = __ballot_sync(0xffffffffu, k);
+    if (nxt == alive) break;
+    alive = nxt;
+  }
+  if (__any_sync(0xffffffffu, unc)) return warp_hull_small<V>(P, m, dst);
+  __syncwarp();
+  if ((alive >> lane) & 1u) dst[__popc(alive & ((1u << lane) - 1u))] = q;
+  __syncwarp();
+  return __popc(alive);
+}
+
 // Many survivors (arc-like input, an instance edge): the warp hulls 32 runs
 // of SB in parallel, merges them with a warp merge tree and bridges the block
 // hood into the running hood (spilling it to HBM when it outgrows Hs).
@@ -2001,7 +2028,9 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
         // instances): hull them with the warp -- straight into the output
         // slots when no anchor point is needed (whole instances)
         written = spi == 1;
-        hs.n = pend ? warp_hull_small<V>(PBf, pend, written ? gout + ubase : Hs) : 0;
+        V* const hd = written ? gout + ubase : Hs;
+        if constexpr (LEAN) hs.n = pend ? (pend <= 32 ? warp_hull_small32<V>(PBf, pend, hd) : warp_hull_small<V>(PBf, pend, hd)) : 0;
+        else hs.n = pend ? warp_hull_small<V>(PBf, pend, hd) : 0;
         pend = 0;
       } else {
         flush();
