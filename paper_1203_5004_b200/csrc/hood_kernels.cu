@@ -2029,7 +2029,8 @@ __global__ void __maxnreg__(LEAN ? HOOD_LEAN_NREG : HOOD_RING_MAXNREG) ring_hull
         // slots when no anchor point is needed (whole instances)
         written = spi == 1;
         V* const hd = written ? gout + ubase : Hs;
-        if constexpr (LEAN) hs.n = pend ? (pend <= 32 ? warp_hull_small32<V>(PBf, pend, hd) : warp_hull_small<V>(PBf, pend, hd)) : 0;
+        if constexpr (LEAN || sizeof(S) == 4)
+          hs.n = pend ? (pend <= 32 ? warp_hull_small32<V>(PBf, pend, hd) : warp_hull_small<V>(PBf, pend, hd)) : 0;
         else hs.n = pend ? warp_hull_small<V>(PBf, pend, hd) : 0;
         pend = 0;
       } else {
