@@ -36,7 +36,10 @@ struct DevError {
 constexpr unsigned long long kTripleKey = 1ULL << 62;
 
 // parts of a unit under tail stealing: the owner's and up to 3 stolen tails
-constexpr int kStealParts = 4;
+#ifndef HOOD_STEAL_PARTS
+#define HOOD_STEAL_PARTS 4
+#endif
+constexpr int kStealParts = HOOD_STEAL_PARTS;
 
 template <class S>
 struct SlabParams {
